@@ -1,0 +1,186 @@
+/*
+ * wv.h -- C ABI of libwv.so, the B200 (sm_100a) Wolstenholme / Vandiver
+ * residue search (Hathi, Mossinghoff, Trudgian, arXiv:2101.11157).
+ *
+ * Citations: "P:Lnnn" = /root/reference/PAPER.md line nnn with its section /
+ * equation label; readings R1..R6 are listed in DESIGN.md.
+ *
+ * What the library computes (BASELINE.json north_star):
+ * for every prime p with lo <= p < hi and p >= 5,
+ *   W:  B_{p-3} mod p   (Bernoulli, z/(e^z-1) convention), via
+ *       L_W B_{p-3} == sum_i a_i sum_{x_i p < s < y_i p} s^{-3}   (mod p)
+ *       -- eqnBB1/2/6/9/16/22/30, eqnV12 at p = 7;
+ *   V:  E_{p-3} mod p   (Euler, sec z convention; reading R1), via
+ *       L_V E_{p-3} == sum_i a_i sum_{x_i p < s < y_i p} s^{-2}   (mod p)
+ *       -- eqnEE3/5/9/16/24/33;
+ * each inner sum evaluated by the (c0, c1) product recurrence eqnComputeS
+ * and partial pairs merged by eqnCombinePairs.
+ * A prime is a hit when its residue is 0 (Wolstenholme prime: p | B_{p-3},
+ * P:L59-66; Vandiver prime: p | E_{p-3}).
+ *
+ * Conventions for every entry point:
+ *  - integers are host-endian; residues are canonical in [0, p);
+ *    WV_RES_NONE marks a test that was not requested;
+ *  - ranges are half-open [lo, hi); primes < 5 are skipped; hi <= 2^62;
+ *  - outputs are sorted ascending by p and identical for every shard count,
+ *    block size and internal partition (the combine is exact);
+ *  - the library never keeps caller pointers after a call returns;
+ *  - all device work runs on the current CUDA device; device entry points
+ *    run on the caller's stream, host entry points on an internal stream;
+ *  - on a non-OK return, wv_last_error() gives a thread-local message.
+ * There is no CPU fallback: without a usable sm_100 GPU every compute entry
+ * point returns WV_ECUDA.
+ */
+#ifndef WV_H
+#define WV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- codes */
+#define WV_MODE_W    1u   /* Wolstenholme test: B_{p-3} mod p */
+#define WV_MODE_V    2u   /* Vandiver test:     E_{p-3} mod p */
+#define WV_MODE_BOTH 3u
+
+#define WV_OK        0
+#define WV_EINVAL   (-1)  /* lo >= hi, hi > 2^62, mode not in {1,2,3}, shard >= nshards, bad id */
+#define WV_ENOSPC   (-2)  /* a caller capacity is too small; the *n_ outputs hold the sizes needed */
+#define WV_ECUDA    (-3)  /* CUDA error (message in wv_last_error) */
+#define WV_ENOMEM   (-4)  /* device allocation failed */
+
+#define WV_RES_NONE UINT64_MAX
+#define WV_HI_MAX   (UINT64_C(1) << 62)
+
+#define WV_HIT_W 1u       /* p | numerator of B_{p-3}: Wolstenholme prime */
+#define WV_HIT_V 2u       /* p | E_{p-3}: Vandiver prime */
+
+typedef struct { uint64_t p; uint32_t flags; uint32_t reserved; } wv_hit;
+typedef struct { uint64_t p; uint64_t res_w; uint64_t res_v; } wv_residue;
+
+/* --------------------------------------------------------- host buffers */
+
+/* wv_search: the whole hot path over [lo, hi) on the current device.
+ *   out_hits[0..*n_hits)       primes with a zero residue and which test(s);
+ *   out_residues[0..*n_primes) every prime with its residues (may be NULL:
+ *                              then res_cap is ignored and only hits are returned).
+ * Buffers are caller-owned host memory (pinned or pageable).  Two-call sizing:
+ * if hits_cap < hits or (out_residues && res_cap < primes), returns WV_ENOSPC
+ * with *n_hits / *n_primes set to the required counts and writes nothing else.
+ * Device scratch is allocated (stream-ordered) and freed inside the call. */
+int wv_search(uint64_t lo, uint64_t hi, uint32_t mode,
+              wv_hit *out_hits, size_t hits_cap, size_t *n_hits,
+              wv_residue *out_residues, size_t res_cap, size_t *n_primes);
+
+/* wv_search_shard: as wv_search, restricted to this shard's blocks.  [lo, hi)
+ * is cut into blocks of `block` integers (0 = default: a power of two giving
+ * every shard >= 32 blocks, at least 2^16); block b = [lo + b*block, ...)
+ * belongs to shard b mod nshards (interleaved).  *checksum
+ * receives this shard's order-independent 64-bit checksum (wv_checksum_term
+ * summed mod 2^64), so shard checksums add up to the unsharded one.
+ * checksum may be NULL. */
+int wv_search_shard(uint64_t lo, uint64_t hi, uint32_t mode,
+                    uint32_t shard, uint32_t nshards, uint64_t block,
+                    wv_hit *out_hits, size_t hits_cap, size_t *n_hits,
+                    wv_residue *out_residues, size_t res_cap, size_t *n_primes,
+                    uint64_t *checksum);
+
+/* ------------------------------------------------------- device buffers */
+
+/* Device-resident form of the same path (what bench.py's `value` times).
+ * wv_device_workspace_bytes: bytes of device workspace wv_search_device needs
+ * for these arguments (an upper bound fixed by (lo, hi, mode, shard, nshards,
+ * block); it does not depend on the data) and the prime capacity the outputs
+ * must have (*prime_cap, an upper bound on the primes in this shard from the
+ * Montgomery-Vaughan bound pi(x+y)-pi(x) < 2y/log y). */
+int wv_device_workspace_bytes(uint64_t lo, uint64_t hi, uint32_t mode,
+                              uint32_t shard, uint32_t nshards, uint64_t block,
+                              size_t *workspace_bytes, size_t *prime_cap);
+
+/* wv_search_device: all pointers are device pointers (e.g. torch tensors).
+ *   d_primes[prime_cap]   uint64 primes, ascending;
+ *   d_res_w[prime_cap]    uint64 B_{p-3} mod p   (WV_RES_NONE if not requested);
+ *   d_res_v[prime_cap]    uint64 E_{p-3} mod p   (WV_RES_NONE if not requested);
+ *   d_hits[prime_cap]     wv_hit, ascending (may be NULL);
+ *   d_checksum[1]         uint64 checksum of this shard (may be NULL);
+ *   d_workspace           >= wv_device_workspace_bytes(...) bytes, 256-byte aligned
+ *                         (NULL: the library allocates it stream-ordered);
+ *   stream                a cudaStream_t (NULL = legacy default stream).
+ * On return, *n_primes and *n_hits (host) hold the counts; the stream has been
+ * synchronised (the counts are needed on the host).  Returns WV_ENOSPC if
+ * prime_cap or workspace_bytes is too small (nothing written). */
+int wv_search_device(uint64_t lo, uint64_t hi, uint32_t mode,
+                     uint32_t shard, uint32_t nshards, uint64_t block,
+                     uint64_t *d_primes, uint64_t *d_res_w, uint64_t *d_res_v,
+                     wv_hit *d_hits, uint64_t *d_checksum, size_t prime_cap,
+                     void *d_workspace, size_t workspace_bytes, void *stream,
+                     size_t *n_primes, size_t *n_hits);
+
+/* wv_residues_device: the residue step alone for a caller-supplied list of
+ * primes d_primes[0..n) (each >= 5, < 2^62, need not be sorted or distinct;
+ * composite inputs give meaningless values).  Writes d_res_w[i], d_res_v[i]
+ * as above.  Workspace as for wv_search_device, sized by
+ * wv_residues_workspace_bytes(n, max_p, mode, ...). */
+int wv_residues_workspace_bytes(size_t n, uint64_t max_p, uint32_t mode, size_t *workspace_bytes);
+int wv_residues_device(const uint64_t *d_primes, size_t n, uint32_t mode,
+                       uint64_t *d_res_w, uint64_t *d_res_v,
+                       void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* wv_sieve_device: the sieve step alone: primes q with
+ * max(lo,5) <= q < hi into d_primes[0..*n) ascending.  Returns WV_ENOSPC with
+ * *n = count if cap is too small. */
+int wv_sieve_device(uint64_t lo, uint64_t hi, uint64_t *d_primes, size_t cap, size_t *n,
+                    void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* wv_prime_count: number of primes q with max(lo,5) <= q < hi, counted by the
+ * same segmented sieve without materialising them (used to pin the sieve to
+ * the paper's counts).  Device scratch is internal. */
+int wv_prime_count(uint64_t lo, uint64_t hi, uint64_t *count);
+
+/* ------------------------------------------------------ small utilities */
+
+/* Checksum term of one prime (reading R6 in DESIGN.md):
+ * mix64(p ^ rotl(res_w, 21) ^ rotl(res_v, 42)), mix64 = splitmix64 finaliser.
+ * Checksums are sums of terms mod 2^64. */
+uint64_t wv_checksum_term(uint64_t p, uint64_t res_w, uint64_t res_v);
+
+/* Congruence table (host copy of the constants the kernels use).
+ * id 0..wv_congruence_count()-1.  Each congruence states
+ *   L * X == sum_{j<m} a_j * S(xn_j/xd_j, yn_j/yd_j)  (mod p),
+ * S(x,y) = sum_{xp<s<yp} s^{-e}; X = B_{p-3} (e = 3) or E_{p-3} (e = 2).
+ * Valid for p >= min_p and p != excluded_p.  Returns WV_EINVAL for a bad id. */
+typedef struct { int64_t a; uint32_t xn, xd, yn, yd; } wv_term;
+typedef struct {
+    char     name[8];       /* "BB30", "EE33", "VOR12", ... */
+    int64_t  L;             /* left factor */
+    uint32_t e;             /* 3: B_{p-3} (s^-3);  2: E_{p-3} (s^-2) */
+    uint32_t m;             /* number of sums */
+    uint32_t min_p;
+    uint32_t excluded_p;    /* 0 = none */
+    wv_term  t[33];
+} wv_congruence;
+int wv_congruence_count(void);
+int wv_congruence_get(int id, wv_congruence *out);
+
+/* Schedule override for tests and benchmarking (process-global, not
+ * thread-safe): force congruence ids for W and V (-1 restores the default
+ * schedule).  The caller must respect validity (min_p / excluded_p); an
+ * invalid forced choice for some p gives WV_EINVAL from the search. */
+int wv_set_schedule_override(int w_id, int v_id);
+/* Default schedule: W: p = 5 BB1, p = 7 VOR12, 11 <= p < 4096 BB1, p >= 4096 BB30;
+ *                   V: p < 4096 EE3, p >= 4096 EE33.  Returns the id used. */
+int wv_schedule(uint64_t p, uint32_t test /* WV_MODE_W or WV_MODE_V */);
+
+/* Counters: kernels launched by this library since load (process-wide). */
+uint64_t wv_launch_count(void);
+/* Library / device info string (build flags, sm, ...). */
+const char *wv_version(void);
+const char *wv_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WV_H */

@@ -1,1 +1,18 @@
-"""B200-native Wolstenholme / Vandiver residue search (arXiv:2101.11157 hot path)."""
+"""B200-native Wolstenholme / Vandiver residue search (arXiv:2101.11157 hot path).
+
+Public API (thin binding over the C ABI in include/wv.h, implemented by the
+CUDA library libwv.so built from csrc/):
+
+    search(lo, hi, mode)                   -> (hits, residues)      host buffers
+    search_shard(lo, hi, mode, s, n, blk)  -> (hits, residues, checksum)
+    DeviceSearch(lo, hi, mode).run()       device-resident buffers (torch)
+    residues_device(primes_tensor, mode)   residue step only
+    sieve_device(lo, hi)                   sieve step only
+    congruences(), schedule(p, test), set_schedule_override(w, v)
+
+Residues are canonical in [0, p): B_{p-3} mod p (mode W) and E_{p-3} mod p in
+the secant convention (mode V).  ``workloads`` holds the BASELINE configs.
+"""
+from ._wv import (HIT_DTYPE, HIT_V, HIT_W, MODE_BOTH, MODE_V, MODE_W, RES_DTYPE, RES_NONE, DeviceSearch,  # noqa: F401
+                  WVError, checksum_term, congruences, launch_count, lib, prime_count, residues_device, residues_of, schedule,
+                  search, search_shard, set_schedule_override, sieve_device, version)

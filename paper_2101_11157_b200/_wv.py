@@ -1,0 +1,247 @@
+"""Thin ctypes binding over libwv.so (include/wv.h) -- argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; this module only
+converts Python ints / numpy arrays / torch tensors to pointers and back.
+There is no CPU fallback: if libwv.so is missing or the device is not an
+sm_100 GPU, calls raise WVError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwv.so")
+
+MODE_W, MODE_V, MODE_BOTH = 1, 2, 3
+RES_NONE = (1 << 64) - 1
+WV_OK, WV_EINVAL, WV_ENOSPC, WV_ECUDA, WV_ENOMEM = 0, -1, -2, -3, -4
+HIT_W, HIT_V = 1, 2
+
+HIT_DTYPE = np.dtype([("p", "<u8"), ("flags", "<u4"), ("reserved", "<u4")])
+RES_DTYPE = np.dtype([("p", "<u8"), ("res_w", "<u8"), ("res_v", "<u8")])
+
+
+class WVError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libwv error {code}: {msg}")
+        self.code = code
+
+
+class _Term(ctypes.Structure):
+    _fields_ = [("a", ctypes.c_int64), ("xn", ctypes.c_uint32), ("xd", ctypes.c_uint32),
+                ("yn", ctypes.c_uint32), ("yd", ctypes.c_uint32)]
+
+
+class _Cong(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 8), ("L", ctypes.c_int64), ("e", ctypes.c_uint32),
+                ("m", ctypes.c_uint32), ("min_p", ctypes.c_uint32), ("excluded_p", ctypes.c_uint32),
+                ("t", _Term * 33)]
+
+
+# (name, restype, argtypes) for every symbol include/wv.h declares
+_u64, _u32, _sz, _vp, _i = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int
+_P = ctypes.POINTER
+SIGNATURES = {
+    "wv_search": (_i, [_u64, _u64, _u32, _vp, _sz, _P(_sz), _vp, _sz, _P(_sz)]),
+    "wv_search_shard": (_i, [_u64, _u64, _u32, _u32, _u32, _u64, _vp, _sz, _P(_sz), _vp, _sz, _P(_sz), _P(_u64)]),
+    "wv_device_workspace_bytes": (_i, [_u64, _u64, _u32, _u32, _u32, _u64, _P(_sz), _P(_sz)]),
+    "wv_search_device": (_i, [_u64, _u64, _u32, _u32, _u32, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _sz, _vp,
+                              _P(_sz), _P(_sz)]),
+    "wv_residues_workspace_bytes": (_i, [_sz, _u64, _u32, _P(_sz)]),
+    "wv_residues_device": (_i, [_vp, _sz, _u32, _vp, _vp, _vp, _sz, _vp]),
+    "wv_sieve_device": (_i, [_u64, _u64, _vp, _sz, _P(_sz), _vp, _sz, _vp]),
+    "wv_prime_count": (_i, [_u64, _u64, _P(_u64)]),
+    "wv_checksum_term": (_u64, [_u64, _u64, _u64]),
+    "wv_congruence_count": (_i, []),
+    "wv_congruence_get": (_i, [_i, _P(_Cong)]),
+    "wv_set_schedule_override": (_i, [_i, _i]),
+    "wv_schedule": (_i, [_u64, _u32]),
+    "wv_launch_count": (_u64, []),
+    "wv_version": (ctypes.c_char_p, []),
+    "wv_last_error": (ctypes.c_char_p, []),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libwv.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != WV_OK:
+        raise WVError(rc, lib().wv_last_error().decode(errors="replace"))
+
+
+def _ptr(t):
+    """Device/host pointer of a torch tensor or numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return ctypes.c_void_p(t.data_ptr())
+    return t.ctypes.data_as(ctypes.c_void_p)
+
+
+# ------------------------------------------------------------------ host-buffer API
+def search(lo: int, hi: int, mode: int = MODE_BOTH, residues: bool = True):
+    """wv_search: returns (hits: np.ndarray[HIT_DTYPE], residues: np.ndarray[RES_DTYPE] or None)."""
+    return search_shard(lo, hi, mode, 0, 1, 0, residues)[:2]
+
+
+def search_shard(lo: int, hi: int, mode: int, shard: int, nshards: int, block: int = 0, residues: bool = True):
+    """wv_search_shard: returns (hits, residues or None, checksum)."""
+    L = lib()
+    ws, cap = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(L.wv_device_workspace_bytes(lo, hi, mode, shard, nshards, block, ctypes.byref(ws), ctypes.byref(cap)))
+    n = max(int(cap.value), 1)
+    hits = np.zeros(n, dtype=HIT_DTYPE)
+    res = np.zeros(n, dtype=RES_DTYPE) if residues else None
+    nh, npr, chk = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_uint64()
+    _check(L.wv_search_shard(lo, hi, mode, shard, nshards, block, _ptr(hits), n, ctypes.byref(nh), _ptr(res),
+                             n if residues else 0, ctypes.byref(npr), ctypes.byref(chk)))
+    return hits[: nh.value].copy(), (res[: npr.value].copy() if residues else None), int(chk.value)
+
+
+# ------------------------------------------------------------------ device API (torch tensors)
+class DeviceSearch:
+    """Preallocated device buffers (torch) for repeated wv_search_device calls on one window."""
+
+    def __init__(self, lo, hi, mode=MODE_BOTH, shard=0, nshards=1, block=0, device=None):
+        import torch
+        L = lib()
+        ws, cap = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(L.wv_device_workspace_bytes(lo, hi, mode, shard, nshards, block, ctypes.byref(ws), ctypes.byref(cap)))
+        self.args = (lo, hi, mode, shard, nshards, block)
+        self.device = torch.device(device or "cuda")
+        self.cap = max(int(cap.value), 1)
+        self.ws_bytes = int(ws.value)
+        u = dict(dtype=torch.int64, device=self.device)      # uint64 bit patterns
+        self.primes = torch.empty(self.cap, **u)
+        self.res_w = torch.empty(self.cap, **u)
+        self.res_v = torch.empty(self.cap, **u)
+        self.hits = torch.empty(self.cap * 2, **u)          # wv_hit = 16 bytes
+        self.checksum = torch.zeros(1, **u)
+        self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.n_primes = 0
+        self.n_hits = 0
+
+    def run(self, stream=None):
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        npr, nh = ctypes.c_size_t(), ctypes.c_size_t()
+        lo, hi, mode, shard, nshards, block = self.args
+        _check(lib().wv_search_device(lo, hi, mode, shard, nshards, block, _ptr(self.primes), _ptr(self.res_w),
+                                      _ptr(self.res_v), _ptr(self.hits), _ptr(self.checksum), self.cap,
+                                      _ptr(self.workspace), self.ws_bytes, ctypes.c_void_p(st.cuda_stream),
+                                      ctypes.byref(npr), ctypes.byref(nh)))
+        self.n_primes, self.n_hits = int(npr.value), int(nh.value)
+        return self
+
+    # host views (copies) of the outputs
+    def primes_np(self):
+        return self.primes[: self.n_primes].cpu().numpy().view(np.uint64)
+
+    def res_np(self):
+        return (self.res_w[: self.n_primes].cpu().numpy().view(np.uint64),
+                self.res_v[: self.n_primes].cpu().numpy().view(np.uint64))
+
+    def hits_np(self):
+        raw = self.hits[: 2 * self.n_hits].cpu().numpy().view(np.uint8)
+        return np.frombuffer(raw.tobytes(), dtype=HIT_DTYPE)
+
+    def checksum_int(self):
+        return int(self.checksum.cpu().numpy().view(np.uint64)[0])
+
+
+def residues_device(primes, mode=MODE_BOTH, stream=None):
+    """wv_residues_device on a torch uint64/int64 cuda tensor of primes -> (res_w, res_v) tensors."""
+    import torch
+    n = primes.numel()
+    ws = ctypes.c_size_t()
+    _check(lib().wv_residues_workspace_bytes(n, 0, mode, ctypes.byref(ws)))
+    work = torch.empty(max(int(ws.value), 1), dtype=torch.uint8, device=primes.device)
+    rw = torch.empty_like(primes)
+    rv = torch.empty_like(primes)
+    st = stream if stream is not None else torch.cuda.current_stream(primes.device)
+    _check(lib().wv_residues_device(_ptr(primes), n, mode, _ptr(rw), _ptr(rv), _ptr(work), int(ws.value),
+                                    ctypes.c_void_p(st.cuda_stream)))
+    return rw, rv
+
+
+def residues_of(plist, mode=MODE_BOTH, device="cuda"):
+    """Convenience: residues for a Python list of primes -> (np res_w, np res_v)."""
+    import torch
+    arr = np.asarray(plist, dtype=np.uint64)
+    t = torch.from_numpy(arr.view(np.int64)).to(device)
+    rw, rv = residues_device(t, mode)
+    torch.cuda.synchronize()
+    return rw.cpu().numpy().view(np.uint64), rv.cpu().numpy().view(np.uint64)
+
+
+def sieve_device(lo, hi, device="cuda"):
+    """wv_sieve_device -> np.ndarray of primes in [max(lo,5), hi)."""
+    import torch
+    L = lib()
+    ws, cap = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(L.wv_device_workspace_bytes(lo, hi, 1, 0, 1, 0, ctypes.byref(ws), ctypes.byref(cap)))
+    out = torch.empty(max(int(cap.value), 1), dtype=torch.int64, device=device)
+    work = torch.empty(int(ws.value), dtype=torch.uint8, device=device)
+    n = ctypes.c_size_t()
+    st = torch.cuda.current_stream(out.device)
+    _check(L.wv_sieve_device(lo, hi, _ptr(out), int(cap.value), ctypes.byref(n), _ptr(work), int(ws.value),
+                             ctypes.c_void_p(st.cuda_stream)))
+    return out[: n.value].cpu().numpy().view(np.uint64)
+
+
+def prime_count(lo, hi):
+    """wv_prime_count: primes in [max(lo,5), hi) counted on the device."""
+    c = ctypes.c_uint64()
+    _check(lib().wv_prime_count(lo, hi, ctypes.byref(c)))
+    return int(c.value)
+
+
+# ------------------------------------------------------------------ small utilities
+def checksum_term(p, rw, rv):
+    return int(lib().wv_checksum_term(p, rw, rv))
+
+
+def congruences():
+    """The library's congruence table as a list of dicts."""
+    L = lib()
+    out = []
+    for i in range(L.wv_congruence_count()):
+        c = _Cong()
+        _check(L.wv_congruence_get(i, ctypes.byref(c)))
+        out.append(dict(id=i, name=c.name.decode(), L=c.L, e=c.e, min_p=c.min_p, excluded_p=c.excluded_p,
+                        terms=[(c.t[j].a, c.t[j].xn, c.t[j].xd, c.t[j].yn, c.t[j].yd) for j in range(c.m)]))
+    return out
+
+
+def set_schedule_override(w_id=-1, v_id=-1):
+    _check(lib().wv_set_schedule_override(w_id, v_id))
+
+
+def schedule(p, test):
+    return int(lib().wv_schedule(p, test))
+
+
+def launch_count():
+    return int(lib().wv_launch_count())
+
+
+def version():
+    return lib().wv_version().decode()

@@ -1,0 +1,684 @@
+// wv_api.cu -- host runtime and C ABI of libwv.so (declared in include/wv.h).
+//
+// Host-side responsibilities only: argument checks, workspace layout, the
+// launch sequence (sieve -> plan -> scan -> residue -> finalize -> flags/hits),
+// batching of the partial-pair buffer, and host<->device copies for the
+// host-buffer entry points.  Every arithmetic step of the method runs in the
+// kernels of wv_sieve.cuh / wv_residue.cuh.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "../../include/wv.h"
+#include "wv_mont.cuh"
+#include "wv_residue.cuh"
+#include "wv_scan.cuh"
+#include "wv_sieve.cuh"
+
+using namespace wv;
+
+// ------------------------------------------------------------------ constants
+#define WV_CONG(NAME, L, E, M, MINP, EXCL, ...) {NAME, (int64_t)(L), E, M, MINP, EXCL, __VA_ARGS__},
+static const Cong h_cong[NCONG] = {
+#include "congruences.inc"
+};
+#undef WV_CONG
+
+// odd primes below 256: the bootstrap list that sieves [3, 65536)
+static const uint32_t h_boot[] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59, 61, 67,
+                                  71, 73, 79, 83, 89, 97, 101, 103, 107, 109, 113, 127, 131, 137, 139,
+                                  149, 151, 157, 163, 167, 173, 179, 181, 191, 193, 197, 199, 211, 223,
+                                  227, 229, 233, 239, 241, 251};
+static const uint64_t BASE0_HI = 65536;
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[1024] = "";
+static std::atomic<uint64_t> g_launches{0};
+static Sched g_sched = {4096, C_BB1, C_BB30, C_EE3, C_EE33, -1, -1};
+
+static int set_err(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CK(x)                                                                                        \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            return set_err(e_ == cudaErrorMemoryAllocation ? WV_ENOMEM : WV_ECUDA, "%s:%d %s: %s",   \
+                           __FILE__, __LINE__, #x, cudaGetErrorString(e_));                          \
+    } while (0)
+#define TRY(x)                       \
+    do {                             \
+        int r_ = (x);                \
+        if (r_ != WV_OK) return r_;  \
+    } while (0)
+#define LAUNCH(kern, grid, block, st, ...)                          \
+    do {                                                            \
+        kern<<<(grid), (block), 0, (st)>>>(__VA_ARGS__);            \
+        g_launches.fetch_add(1, std::memory_order_relaxed);         \
+        CK(cudaGetLastError());                                     \
+    } while (0)
+
+// ------------------------------------------------------------------ device context
+struct DevCtx {
+    bool ready = false;
+    int sms = 0;
+    int occ32 = 0, occ64 = 0;
+    uint32_t *d_base0 = nullptr;   // odd primes < 65536
+    uint32_t nbase0 = 0;
+    cudaStream_t stream = nullptr; // internal stream for the host-buffer API
+};
+static DevCtx g_ctx[64];
+static std::mutex g_mu;
+
+static int ctx_get(DevCtx **out) {
+    int dev = -1;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return set_err(WV_ECUDA, "device index %d out of range", dev);
+    DevCtx &c = g_ctx[dev];
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!c.ready) {
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major != 10)
+            return set_err(WV_ECUDA, "libwv.so is built for sm_100a; device %d is sm_%d%d", dev, prop.major, prop.minor);
+        c.sms = prop.multiProcessorCount;
+        CK(cudaMemcpyToSymbol(c_cong, h_cong, sizeof h_cong));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ32, residue_kernel<Mont32>, RES_THREADS, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ64, residue_kernel<Mont64>, RES_THREADS, 0));
+        if (c.occ32 < 1) c.occ32 = 1;
+        if (c.occ64 < 1) c.occ64 = 1;
+        CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        // level-0 base primes: odd primes in [3, 65536), sieved on the device
+        const uint32_t nboot = sizeof h_boot / sizeof h_boot[0];
+        uint32_t *d_boot, *d_bitmap;
+        uint64_t *d_cnt, *d_off, *d_tiles;
+        const uint64_t nseg = BASE0_HI / SIEVE_SPAN;  // 1 segment for [0, 65536)
+        const uint64_t nseg1 = nseg > 0 ? nseg : 1;
+        CK(cudaMalloc(&d_boot, sizeof h_boot));
+        CK(cudaMalloc(&d_bitmap, nseg1 * SIEVE_WORDS * 4));
+        CK(cudaMalloc(&d_cnt, nseg1 * 8));
+        CK(cudaMalloc(&d_off, (nseg1 + 1) * 8));
+        CK(cudaMalloc(&d_tiles, 64));
+        CK(cudaMemcpy(d_boot, h_boot, sizeof h_boot, cudaMemcpyHostToDevice));
+        SegMap m{0, BASE0_HI, SIEVE_SPAN, 0, 1, 1, 3};
+        cudaStream_t st = c.stream;
+        LAUNCH(sieve_segments_kernel, 1, SIEVE_THREADS, st, m, d_boot, nboot, nullptr, d_bitmap, d_cnt);
+        LAUNCH(scan_tile_totals<uint64_t>, 1, SCAN_THREADS, st, d_cnt, (uint64_t)1, d_tiles);
+        LAUNCH(scan_tiles_single, 1, SCAN_THREADS, st, d_tiles, (uint64_t)1, d_off + 1);
+        LAUNCH(scan_tile_apply<uint64_t>, 1, SCAN_THREADS, st, d_cnt, (uint64_t)1, d_tiles, d_off);
+        uint64_t nb = 0;
+        CK(cudaMemcpyAsync(&nb, d_off + 1, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaMalloc(&c.d_base0, nb * 4));
+        LAUNCH(sieve_write_kernel<uint32_t>, 1, SIEVE_THREADS, st, m, d_bitmap, d_off, c.d_base0, nb);
+        CK(cudaStreamSynchronize(st));
+        c.nbase0 = (uint32_t)nb;
+        cudaFree(d_boot); cudaFree(d_bitmap); cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_tiles);
+        if (nb != 6541) return set_err(WV_ECUDA, "base-prime sieve produced %llu primes < 65536 (want 6541)",
+                                       (unsigned long long)nb);
+        c.ready = true;
+    }
+    *out = &c;
+    return WV_OK;
+}
+
+// ------------------------------------------------------------------ sizes
+static uint64_t isqrt64(uint64_t x) {
+    uint64_t r = (uint64_t)sqrtl((long double)x);
+    while (r * r > x) r--;
+    while ((r + 1) * (r + 1) <= x) r++;
+    return r;
+}
+
+// upper bound on the primes in an interval of y integers: Montgomery-Vaughan
+// pi(x+y) - pi(x) < 2y / log y, and trivially <= y/2 + 1 (odd numbers) + 1.
+static uint64_t prime_bound(uint64_t y) {
+    if (y == 0) return 0;
+    uint64_t triv = y / 2 + 2;
+    if (y < 64) return triv;
+    uint64_t mv = (uint64_t)(2.0 * (double)y / log((double)y)) + 2;
+    return mv < triv ? mv : triv;
+}
+
+static uint64_t ntiles(uint64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 1; }
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static const uint64_t PART_BUDGET = 1ull << 24;   // partial pairs per batch (256 MiB)
+
+enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2, M_CNT32 = 3, M_CNT64 = 4, M_NHITS = 5, M_CHECKSUM = 6,
+       M_NBASE1 = 7, M_SPLIT = 8 /* 2 slots */, M_SLOTS = 16 };
+
+struct Layout {
+    // problem
+    uint64_t lo, hi, block;
+    uint32_t mode, shard, nshards, ntests;
+    SegMap map, map1;
+    uint64_t nseg, nseg1, nbase1_cap;
+    bool need_l1;
+    uint64_t prime_cap, K;
+    // offsets into the workspace
+    size_t o_misc, o_bitmap, o_segcnt, o_segoff, o_tiles, o_base1, o_recs, o_nch, o_start, o_part,
+           o_flags, o_pos, o_kb, total;
+    uint64_t tiles_n;
+};
+
+static void layout_tail(Layout &L) {
+    size_t o = L.total;
+    L.o_recs = o;  o += al(L.K * sizeof(Rec));
+    L.o_nch = o;   o += al(L.K * 8);
+    L.o_start = o; o += al((L.K + 1) * 8);
+    L.o_part = o;  o += al(PART_BUDGET * sizeof(ulonglong2));
+    L.o_kb = o;    o += al(2 * (L.K * CAP_CHUNKS / (PART_BUDGET / 2) + 4) * 8);
+    uint64_t t = ntiles(L.K + 1);
+    if (ntiles(L.prime_cap) > t) t = ntiles(L.prime_cap);
+    if (L.tiles_n < t) L.tiles_n = t;
+    L.o_tiles = o; o += al(L.tiles_n * 8);
+    L.total = o;
+}
+
+static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, uint32_t nshards, uint64_t block,
+                       Layout &L) {
+    if (hi <= lo) return set_err(WV_EINVAL, "empty or inverted range [%llu, %llu)", (unsigned long long)lo,
+                                 (unsigned long long)hi);
+    if (hi > WV_HI_MAX) return set_err(WV_EINVAL, "hi > 2^62");
+    if (mode < 1 || mode > 3) return set_err(WV_EINVAL, "mode %u not in {1,2,3}", mode);
+    if (nshards == 0 || shard >= nshards) return set_err(WV_EINVAL, "shard %u of %u", shard, nshards);
+    const uint64_t width = hi - lo;
+    if (block == 0) {
+        if (nshards == 1) {
+            block = (width + SIEVE_SPAN - 1) / SIEVE_SPAN * SIEVE_SPAN;
+        } else {
+            uint64_t t = width / (32ull * nshards);
+            block = SIEVE_SPAN;
+            while (block * 2 <= t) block *= 2;
+        }
+    }
+    if (block % SIEVE_SPAN != 0) return set_err(WV_EINVAL, "block %llu is not a multiple of %d",
+                                                (unsigned long long)block, SIEVE_SPAN);
+    memset(&L, 0, sizeof L);
+    L.lo = lo; L.hi = hi; L.block = block; L.mode = mode; L.shard = shard; L.nshards = nshards;
+    L.ntests = mode == 3 ? 2 : 1;
+    const uint64_t nblocks = (width + block - 1) / block;
+    const uint64_t my_blocks = nblocks > shard ? (nblocks - shard + nshards - 1) / nshards : 0;
+    const uint64_t spb = block / SIEVE_SPAN;
+    L.map = SegMap{lo, hi, block, shard, nshards, spb, 5};
+    L.nseg = my_blocks * spb;
+    // primes in this shard: sum of per-block bounds
+    uint64_t cap = 0;
+    for (uint64_t j = 0; j < my_blocks; j++) {
+        uint64_t bs = lo + ((uint64_t)shard + j * nshards) * block;
+        uint64_t be = bs + block < hi ? bs + block : hi;
+        cap += prime_bound(be - bs);
+    }
+    L.prime_cap = cap;
+    L.K = cap * L.ntests;
+    // base primes: q <= isqrt(hi - 1)
+    const uint64_t r = isqrt64(hi - 1);
+    L.need_l1 = r >= BASE0_HI;
+    if (L.need_l1) {
+        const uint64_t hi1 = r + 1;
+        const uint64_t blk1 = (hi1 + SIEVE_SPAN - 1) / SIEVE_SPAN * SIEVE_SPAN;
+        L.map1 = SegMap{0, hi1, blk1, 0, 1, blk1 / SIEVE_SPAN, 3};
+        L.nseg1 = blk1 / SIEVE_SPAN;
+        L.nbase1_cap = prime_bound(hi1);
+    }
+    size_t o = 0;
+    L.o_misc = o;   o += al(M_SLOTS * 8);
+    const uint64_t nsegmax = L.nseg > L.nseg1 ? L.nseg : L.nseg1;
+    L.o_bitmap = o; o += al(nsegmax * SIEVE_WORDS * 4);
+    L.o_segcnt = o; o += al(nsegmax * 8);
+    L.o_segoff = o; o += al((nsegmax + 1) * 8);
+    L.o_base1 = o;  o += al(L.nbase1_cap * 4);
+    L.o_flags = o;  o += al(L.prime_cap * 4);
+    L.o_pos = o;    o += al((L.prime_cap + 1) * 8);
+    L.tiles_n = ntiles(nsegmax + 1);
+    L.total = o;
+    layout_tail(L);
+    return WV_OK;
+}
+
+// ------------------------------------------------------------------ launch helpers
+template <typename T>
+static int scan_excl(const T *in, uint64_t n, uint64_t *out, uint64_t *total, uint64_t *tiles, cudaStream_t st) {
+    const uint64_t nt = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (nt == 0) {
+        CK(cudaMemsetAsync(total, 0, 8, st));
+        return WV_OK;
+    }
+    LAUNCH(scan_tile_totals<T>, (unsigned)nt, SCAN_THREADS, st, in, n, tiles);
+    LAUNCH(scan_tiles_single, 1, SCAN_THREADS, st, tiles, nt, total);
+    LAUNCH(scan_tile_apply<T>, (unsigned)nt, SCAN_THREADS, st, in, n, tiles, out);
+    return WV_OK;
+}
+
+static char *WS(void *ws, size_t off) { return (char *)ws + off; }
+
+// sieve [map] with a base list -> out (T), count at *d_count
+template <typename T>
+static int run_sieve(const SegMap &map, uint64_t nseg, const uint32_t *base, uint32_t nbase_host,
+                     const uint64_t *nbase_dev, T *out, uint64_t cap, uint64_t *d_count, void *ws,
+                     const Layout &L, cudaStream_t st) {
+    if (nseg == 0) {
+        CK(cudaMemsetAsync(d_count, 0, 8, st));
+        return WV_OK;
+    }
+    uint32_t *bitmap = (uint32_t *)WS(ws, L.o_bitmap);
+    uint64_t *segcnt = (uint64_t *)WS(ws, L.o_segcnt);
+    uint64_t *segoff = (uint64_t *)WS(ws, L.o_segoff);
+    uint64_t *tiles = (uint64_t *)WS(ws, L.o_tiles);
+    LAUNCH(sieve_segments_kernel, (unsigned)nseg, SIEVE_THREADS, st, map, base, nbase_host, nbase_dev, bitmap, segcnt);
+    TRY(scan_excl<uint64_t>(segcnt, nseg, segoff, d_count, tiles, st));
+    LAUNCH(sieve_write_kernel<T>, (unsigned)nseg, SIEVE_THREADS, st, map, bitmap, segoff, out, cap);
+    return WV_OK;
+}
+
+// base list for the main sieve: level 0 (< 65536) or level 1 (<= isqrt(hi-1))
+static int base_list(DevCtx *c, const Layout &L, void *ws, cudaStream_t st, const uint32_t **base,
+                     uint32_t *nbase_host, const uint64_t **nbase_dev) {
+    uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
+    if (!L.need_l1) {
+        *base = c->d_base0; *nbase_host = c->nbase0; *nbase_dev = nullptr;
+        return WV_OK;
+    }
+    uint32_t *b1 = (uint32_t *)WS(ws, L.o_base1);
+    TRY(run_sieve<uint32_t>(L.map1, L.nseg1, c->d_base0, c->nbase0, nullptr, b1, L.nbase1_cap, misc + M_NBASE1, ws,
+                            L, st));
+    *base = b1; *nbase_host = 0; *nbase_dev = misc + M_NBASE1;
+    return WV_OK;
+}
+
+// plan + scan + residue + finalize for records [0, K) of the primes list.
+// n_dev (device count) or n_host gives the number of valid primes.
+static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev, uint64_t n_host, uint64_t K,
+                        uint32_t mode, bool sorted, uint64_t *res_w, uint64_t *res_v, void *ws, const Layout &L,
+                        cudaStream_t st, uint64_t *n_primes_out) {
+    uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
+    Rec *recs = (Rec *)WS(ws, L.o_recs);
+    uint64_t *nch = (uint64_t *)WS(ws, L.o_nch);
+    uint64_t *start = (uint64_t *)WS(ws, L.o_start);
+    ulonglong2 *part = (ulonglong2 *)WS(ws, L.o_part);
+    uint64_t *kb = (uint64_t *)WS(ws, L.o_kb);
+    uint64_t *tiles = (uint64_t *)WS(ws, L.o_tiles);
+    const unsigned grid_plan = (unsigned)((K + 255) / 256 < (uint64_t)c->sms * 32 ? (K + 255) / 256 : c->sms * 32);
+    if (K > 0) {
+        LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs, nch,
+               (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR));
+    }
+    TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
+    LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
+    uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, (split g32, k64)
+    uint64_t hs[2];
+    CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t n = n_dev ? h[0] : n_host;
+    if (n_primes_out) *n_primes_out = n;
+    if ((int)h[1] != 0) return set_err(WV_EINVAL, "schedule chose a congruence not valid for some prime");
+    const uint64_t G = h[2];
+    uint64_t g32 = sorted ? hs[0] : G, k64 = sorted ? hs[1] : K;   // unsorted: both kernels see everything
+    // batches of <= PART_BUDGET partial pairs, cut at record boundaries
+    std::vector<uint64_t> hk, hg;
+    if (G <= PART_BUDGET) {
+        hk = {0, K};
+        hg = {0, G};
+    } else {
+        const uint64_t step = PART_BUDGET / 2;   // every record has <= CAP_CHUNKS << step chunks
+        const uint64_t nb = (G + step - 1) / step;
+        LAUNCH(batch_bounds_kernel, (unsigned)((nb + 256) / 256), 256, st, start, K, step, nb, kb);
+        hk.resize(2 * (nb + 1));
+        CK(cudaMemcpyAsync(hk.data(), kb, 2 * (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        hg.assign(hk.begin() + (nb + 1), hk.end());   // item bounds start[kb[b]]
+        hk.resize(nb + 1);
+    }
+    for (size_t b = 0; b + 1 < hk.size(); b++) {
+        const uint64_t klo = hk[b], khi = hk[b + 1], glo = hg[b], ghi = hg[b + 1];
+        if (khi <= klo) continue;
+        // 32-bit records: items [glo, min(ghi, g32)); 64-bit: [max(glo, g32), ghi)
+        // (unsorted input: both kernels scan the whole batch and skip the other width)
+        const uint64_t a32 = glo, b32 = sorted ? (ghi < g32 ? ghi : g32) : ghi;
+        const uint64_t a64 = sorted ? (glo > g32 ? glo : g32) : glo, b64 = ghi;
+        if (b32 > a32) {
+            CK(cudaMemsetAsync(misc + M_CNT32, 0, 8, st));
+            const uint64_t khi32 = sorted ? (khi < k64 ? khi : k64) : khi;
+            LAUNCH(residue_kernel<Mont32>, c->sms * c->occ32, RES_THREADS, st, recs, start, klo,
+                   khi32 > klo ? khi32 : klo + 1, a32, b32, glo, part, (unsigned long long *)(misc + M_CNT32));
+        }
+        if (b64 > a64) {
+            CK(cudaMemsetAsync(misc + M_CNT64, 0, 8, st));
+            const uint64_t klo64 = sorted ? (klo > k64 ? klo : k64) : klo;
+            LAUNCH(residue_kernel<Mont64>, c->sms * c->occ64, RES_THREADS, st, recs, start, klo64, khi, a64, b64,
+                   glo, part, (unsigned long long *)(misc + M_CNT64));
+        }
+        const uint64_t nrec = khi - klo;
+        uint64_t fb = (nrec * 32 + 255) / 256;
+        if (fb > (uint64_t)c->sms * 16) fb = (uint64_t)c->sms * 16;
+        LAUNCH(finalize_kernel, (unsigned)fb, 256, st, recs, start, klo, khi, glo, part, res_w, res_v);
+    }
+    return WV_OK;
+}
+
+// ------------------------------------------------------------------ device API
+extern "C" int wv_device_workspace_bytes(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, uint32_t nshards,
+                                         uint64_t block, size_t *workspace_bytes, size_t *prime_cap) {
+    Layout L;
+    TRY(make_layout(lo, hi, mode, shard, nshards, block, L));
+    if (workspace_bytes) *workspace_bytes = L.total;
+    if (prime_cap) *prime_cap = L.prime_cap;
+    return WV_OK;
+}
+
+static int search_device_impl(const Layout &L, uint64_t *d_primes, uint64_t *d_res_w, uint64_t *d_res_v,
+                              wv_hit *d_hits, uint64_t *d_checksum, void *ws, cudaStream_t st, size_t *n_primes,
+                              size_t *n_hits) {
+    DevCtx *c;
+    TRY(ctx_get(&c));
+    uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
+    CK(cudaMemsetAsync(misc, 0, M_SLOTS * 8, st));
+    CK(cudaMemsetAsync(misc + M_FIRST64, 0xff, 8, st));
+    const uint32_t *base;
+    uint32_t nbh;
+    const uint64_t *nbd;
+    TRY(base_list(c, L, ws, st, &base, &nbh, &nbd));
+    TRY(run_sieve<uint64_t>(L.map, L.nseg, base, nbh, nbd, d_primes, L.prime_cap, misc + M_NPRIMES, ws, L, st));
+    uint64_t n = 0;
+    TRY(run_residues(c, d_primes, misc + M_NPRIMES, 0, L.K, L.mode, true, d_res_w, d_res_v, ws, L, st, &n));
+    if (n > L.prime_cap) return set_err(WV_ENOSPC, "prime count %llu exceeds bound %llu", (unsigned long long)n,
+                                        (unsigned long long)L.prime_cap);
+    // residues not requested -> WV_RES_NONE; hit flags; checksum
+    uint32_t *flags = (uint32_t *)WS(ws, L.o_flags);
+    uint64_t *pos = (uint64_t *)WS(ws, L.o_pos);
+    uint64_t *tiles = (uint64_t *)WS(ws, L.o_tiles);
+    const uint64_t kmax = L.prime_cap;
+    if (kmax > 0) {
+        unsigned g = (unsigned)((kmax + 255) / 256 < (uint64_t)c->sms * 16 ? (kmax + 255) / 256 : c->sms * 16);
+        LAUNCH(flags_kernel, g, 256, st, d_primes, misc + M_NPRIMES, 0, kmax, d_res_w, d_res_v, L.mode, flags,
+               (unsigned long long *)(misc + M_CHECKSUM));
+        TRY(scan_excl<uint32_t>(flags, kmax, pos, misc + M_NHITS, tiles, st));
+        if (d_hits)
+            LAUNCH(hits_scatter_kernel, g, 256, st, d_primes, misc + M_NPRIMES, kmax, d_res_w, d_res_v, flags, pos,
+                   (HitOut *)d_hits);
+    }
+    if (d_checksum) CK(cudaMemcpyAsync(d_checksum, misc + M_CHECKSUM, 8, cudaMemcpyDeviceToDevice, st));
+    uint64_t nh = 0;
+    CK(cudaMemcpyAsync(&nh, misc + M_NHITS, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n_primes) *n_primes = n;
+    if (n_hits) *n_hits = nh;
+    return WV_OK;
+}
+
+extern "C" int wv_search_device(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, uint32_t nshards,
+                                uint64_t block, uint64_t *d_primes, uint64_t *d_res_w, uint64_t *d_res_v,
+                                wv_hit *d_hits, uint64_t *d_checksum, size_t prime_cap, void *d_workspace,
+                                size_t workspace_bytes, void *stream, size_t *n_primes, size_t *n_hits) {
+    Layout L;
+    TRY(make_layout(lo, hi, mode, shard, nshards, block, L));
+    if (!d_primes || !d_res_w || !d_res_v) return set_err(WV_EINVAL, "null output pointer");
+    if (prime_cap < L.prime_cap) {
+        if (n_primes) *n_primes = L.prime_cap;
+        return set_err(WV_ENOSPC, "prime_cap %zu < required %llu", prime_cap, (unsigned long long)L.prime_cap);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    void *ws = d_workspace;
+    if (ws && workspace_bytes < L.total)
+        return set_err(WV_ENOSPC, "workspace %zu < required %zu bytes", workspace_bytes, L.total);
+    if (!ws) CK(cudaMallocAsync(&ws, L.total, st));
+    int rc = search_device_impl(L, d_primes, d_res_w, d_res_v, d_hits, d_checksum, ws, st, n_primes, n_hits);
+    if (!d_workspace) {
+        cudaFreeAsync(ws, st);
+        cudaStreamSynchronize(st);
+    }
+    return rc;
+}
+
+extern "C" int wv_residues_workspace_bytes(size_t n, uint64_t max_p, uint32_t mode, size_t *workspace_bytes) {
+    (void)max_p;
+    if (mode < 1 || mode > 3) return set_err(WV_EINVAL, "mode %u not in {1,2,3}", mode);
+    Layout L;
+    memset(&L, 0, sizeof L);
+    L.mode = mode;
+    L.ntests = mode == 3 ? 2 : 1;
+    L.prime_cap = n;
+    L.K = (uint64_t)n * L.ntests;
+    L.o_misc = 0;
+    L.total = al(M_SLOTS * 8);
+    L.tiles_n = 1;
+    layout_tail(L);
+    if (workspace_bytes) *workspace_bytes = L.total;
+    return WV_OK;
+}
+
+extern "C" int wv_residues_device(const uint64_t *d_primes, size_t n, uint32_t mode, uint64_t *d_res_w,
+                                  uint64_t *d_res_v, void *d_workspace, size_t workspace_bytes, void *stream) {
+    size_t need;
+    TRY(wv_residues_workspace_bytes(n, 0, mode, &need));
+    if (n == 0) return WV_OK;
+    if (!d_primes || !d_res_w || !d_res_v) return set_err(WV_EINVAL, "null pointer");
+    Layout L;
+    memset(&L, 0, sizeof L);
+    L.mode = mode; L.ntests = mode == 3 ? 2 : 1; L.prime_cap = n; L.K = (uint64_t)n * L.ntests;
+    L.o_misc = 0; L.total = al(M_SLOTS * 8); L.tiles_n = 1;
+    layout_tail(L);
+    cudaStream_t st = (cudaStream_t)stream;
+    void *ws = d_workspace;
+    if (ws && workspace_bytes < L.total) return set_err(WV_ENOSPC, "workspace %zu < %zu", workspace_bytes, L.total);
+    DevCtx *c;
+    TRY(ctx_get(&c));
+    if (!ws) CK(cudaMallocAsync(&ws, L.total, st));
+    uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
+    int rc = WV_OK;
+    do {
+        if (cudaMemsetAsync(misc, 0, M_SLOTS * 8, st) != cudaSuccess ||
+            cudaMemsetAsync(misc + M_FIRST64, 0xff, 8, st) != cudaSuccess) {
+            rc = set_err(WV_ECUDA, "memset failed");
+            break;
+        }
+        rc = run_residues(c, d_primes, nullptr, n, L.K, mode, false, d_res_w, d_res_v, ws, L, st, nullptr);
+        if (rc != WV_OK) break;
+        unsigned g = (unsigned)((n + 255) / 256 < (uint64_t)c->sms * 16 ? (n + 255) / 256 : c->sms * 16);
+        flags_kernel<<<g, 256, 0, st>>>(d_primes, nullptr, n, n, d_res_w, d_res_v, mode, nullptr, nullptr);
+        g_launches.fetch_add(1);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = set_err(WV_ECUDA, "flags_kernel: %s", cudaGetErrorString(e));
+    } while (0);
+    if (!d_workspace) cudaFreeAsync(ws, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == WV_OK) rc = set_err(WV_ECUDA, "stream sync failed");
+    return rc;
+}
+
+extern "C" int wv_sieve_device(uint64_t lo, uint64_t hi, uint64_t *d_primes, size_t cap, size_t *n,
+                               void *d_workspace, size_t workspace_bytes, void *stream) {
+    Layout L;
+    TRY(make_layout(lo, hi, 1, 0, 1, 0, L));
+    cudaStream_t st = (cudaStream_t)stream;
+    void *ws = d_workspace;
+    if (ws && workspace_bytes < L.total) return set_err(WV_ENOSPC, "workspace %zu < %zu", workspace_bytes, L.total);
+    DevCtx *c;
+    TRY(ctx_get(&c));
+    if (!ws) CK(cudaMallocAsync(&ws, L.total, st));
+    uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
+    int rc = WV_OK;
+    uint64_t cnt = 0;
+    do {
+        if (cudaMemsetAsync(misc, 0, M_SLOTS * 8, st) != cudaSuccess) { rc = set_err(WV_ECUDA, "memset"); break; }
+        const uint32_t *base;
+        uint32_t nbh;
+        const uint64_t *nbd;
+        if ((rc = base_list(c, L, ws, st, &base, &nbh, &nbd)) != WV_OK) break;
+        if ((rc = run_sieve<uint64_t>(L.map, L.nseg, base, nbh, nbd, d_primes, cap, misc + M_NPRIMES, ws, L, st)) !=
+            WV_OK)
+            break;
+        if (cudaMemcpyAsync(&cnt, misc + M_NPRIMES, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+            rc = set_err(WV_ECUDA, "copy");
+            break;
+        }
+    } while (0);
+    if (!d_workspace) cudaFreeAsync(ws, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == WV_OK) rc = set_err(WV_ECUDA, "sync");
+    if (rc != WV_OK) return rc;
+    if (n) *n = cnt;
+    if (cnt > cap) return set_err(WV_ENOSPC, "cap %zu < %llu primes", cap, (unsigned long long)cnt);
+    return WV_OK;
+}
+
+extern "C" int wv_prime_count(uint64_t lo, uint64_t hi, uint64_t *count) {
+    Layout L;
+    TRY(make_layout(lo, hi, 1, 0, 1, 0, L));
+    DevCtx *c;
+    TRY(ctx_get(&c));
+    cudaStream_t st = c->stream;
+    // compact workspace: misc, level-1 bitmap only, counts, offsets, base list, tiles
+    const uint64_t nsegmax = L.nseg > L.nseg1 ? L.nseg : L.nseg1;
+    {
+        size_t o = 0;
+        L.o_misc = o;   o += al(M_SLOTS * 8);
+        L.o_bitmap = o; o += al((L.nseg1 + 1) * SIEVE_WORDS * 4);
+        L.o_segcnt = o; o += al(nsegmax * 8);
+        L.o_segoff = o; o += al((nsegmax + 1) * 8);
+        L.o_base1 = o;  o += al(L.nbase1_cap * 4 + 4);
+        L.o_tiles = o;  o += al(ntiles(nsegmax + 1) * 8);
+        L.total = o;
+    }
+    const size_t need = L.total;
+    void *ws = nullptr;
+    CK(cudaMallocAsync(&ws, need, st));
+    uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
+    int rc = WV_OK;
+    uint64_t cnt = 0;
+    do {
+        if (cudaMemsetAsync(misc, 0, M_SLOTS * 8, st) != cudaSuccess) { rc = set_err(WV_ECUDA, "memset"); break; }
+        const uint32_t *base;
+        uint32_t nbh;
+        const uint64_t *nbd;
+        if ((rc = base_list(c, L, ws, st, &base, &nbh, &nbd)) != WV_OK) break;
+        uint64_t *segcnt = (uint64_t *)WS(ws, L.o_segcnt);
+        uint64_t *segoff = (uint64_t *)WS(ws, L.o_segoff);
+        uint64_t *tiles = (uint64_t *)WS(ws, L.o_tiles);
+        if (L.nseg > 0) {
+            sieve_segments_kernel<<<(unsigned)L.nseg, SIEVE_THREADS, 0, st>>>(L.map, base, nbh, nbd, nullptr, segcnt);
+            g_launches.fetch_add(1);
+            if ((rc = scan_excl<uint64_t>(segcnt, L.nseg, segoff, misc + M_NPRIMES, tiles, st)) != WV_OK) break;
+        }
+        if (cudaMemcpyAsync(&cnt, misc + M_NPRIMES, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+            rc = set_err(WV_ECUDA, "copy");
+            break;
+        }
+    } while (0);
+    (void)nsegmax;
+    cudaFreeAsync(ws, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess && rc == WV_OK) rc = set_err(WV_ECUDA, "prime_count: %s", cudaGetErrorString(e));
+    if (rc == WV_OK && count) *count = cnt;
+    return rc;
+}
+
+// ------------------------------------------------------------------ host API
+static int search_host(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, uint32_t nshards, uint64_t block,
+                       wv_hit *out_hits, size_t hits_cap, size_t *n_hits, wv_residue *out_res, size_t res_cap,
+                       size_t *n_primes, uint64_t *checksum) {
+    Layout L;
+    TRY(make_layout(lo, hi, mode, shard, nshards, block, L));
+    DevCtx *c;
+    TRY(ctx_get(&c));
+    cudaStream_t st = c->stream;
+    const uint64_t cap = L.prime_cap > 0 ? L.prime_cap : 1;
+    const size_t bytes = L.total + al(cap * 8) * 3 + al(cap * sizeof(wv_hit)) + al(cap * sizeof(wv_residue)) + 256;
+    char *buf = nullptr;
+    CK(cudaMallocAsync((void **)&buf, bytes, st));
+    size_t o = 0;
+    void *ws = buf + o;           o += L.total;
+    uint64_t *primes = (uint64_t *)(buf + o); o += al(cap * 8);
+    uint64_t *rw = (uint64_t *)(buf + o);     o += al(cap * 8);
+    uint64_t *rv = (uint64_t *)(buf + o);     o += al(cap * 8);
+    wv_hit *hits = (wv_hit *)(buf + o);       o += al(cap * sizeof(wv_hit));
+    ResOut *packed = (ResOut *)(buf + o);     o += al(cap * sizeof(wv_residue));
+    uint64_t *dchk = (uint64_t *)(buf + o);
+    size_t np = 0, nh = 0;
+    int rc = search_device_impl(L, primes, rw, rv, hits, dchk, ws, st, &np, &nh);
+    if (rc == WV_OK) {
+        if (n_primes) *n_primes = np;
+        if (n_hits) *n_hits = nh;
+        if (nh > hits_cap || (out_res && np > res_cap)) {
+            rc = set_err(WV_ENOSPC, "capacity: hits %zu/%zu, residues %zu/%zu", nh, hits_cap, np, res_cap);
+        } else {
+            if (out_res && np > 0) {
+                unsigned g = (unsigned)((np + 255) / 256 < (uint64_t)c->sms * 16 ? (np + 255) / 256 : c->sms * 16);
+                pack_residues_kernel<<<g, 256, 0, st>>>(primes, np, rw, rv, packed);
+                g_launches.fetch_add(1);
+                cudaMemcpyAsync(out_res, packed, np * sizeof(wv_residue), cudaMemcpyDeviceToHost, st);
+            }
+            if (nh > 0) cudaMemcpyAsync(out_hits, hits, nh * sizeof(wv_hit), cudaMemcpyDeviceToHost, st);
+            if (checksum) cudaMemcpyAsync(checksum, dchk, 8, cudaMemcpyDeviceToHost, st);
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e == cudaSuccess) e = cudaGetLastError();
+            if (e != cudaSuccess) rc = set_err(WV_ECUDA, "copy-out: %s", cudaGetErrorString(e));
+        }
+    }
+    cudaFreeAsync(buf, st);
+    cudaStreamSynchronize(st);
+    return rc;
+}
+
+extern "C" int wv_search(uint64_t lo, uint64_t hi, uint32_t mode, wv_hit *out_hits, size_t hits_cap, size_t *n_hits,
+                         wv_residue *out_residues, size_t res_cap, size_t *n_primes) {
+    return search_host(lo, hi, mode, 0, 1, 0, out_hits, hits_cap, n_hits, out_residues, res_cap, n_primes, nullptr);
+}
+
+extern "C" int wv_search_shard(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, uint32_t nshards,
+                               uint64_t block, wv_hit *out_hits, size_t hits_cap, size_t *n_hits,
+                               wv_residue *out_residues, size_t res_cap, size_t *n_primes, uint64_t *checksum) {
+    return search_host(lo, hi, mode, shard, nshards, block, out_hits, hits_cap, n_hits, out_residues, res_cap,
+                       n_primes, checksum);
+}
+
+// ------------------------------------------------------------------ utilities
+extern "C" uint64_t wv_checksum_term(uint64_t p, uint64_t res_w, uint64_t res_v) { return checksum_term(p, res_w, res_v); }
+
+extern "C" int wv_congruence_count(void) { return NCONG; }
+
+extern "C" int wv_congruence_get(int id, wv_congruence *out) {
+    if (id < 0 || id >= NCONG || !out) return set_err(WV_EINVAL, "congruence id %d", id);
+    static_assert(sizeof(wv_congruence) == sizeof(Cong), "wv_congruence layout");
+    memcpy(out, &h_cong[id], sizeof(Cong));
+    return WV_OK;
+}
+
+extern "C" int wv_set_schedule_override(int w_id, int v_id) {
+    if (w_id >= NCONG || v_id >= NCONG) return set_err(WV_EINVAL, "congruence id out of range");
+    if (w_id >= 0 && h_cong[w_id].e != 3) return set_err(WV_EINVAL, "%s is not a Bernoulli congruence", h_cong[w_id].name);
+    if (v_id >= 0 && h_cong[v_id].e != 2) return set_err(WV_EINVAL, "%s is not an Euler congruence", h_cong[v_id].name);
+    g_sched.w_force = w_id < 0 ? -1 : w_id;
+    g_sched.v_force = v_id < 0 ? -1 : v_id;
+    return WV_OK;
+}
+
+extern "C" int wv_schedule(uint64_t p, uint32_t test) {
+    if (test != WV_MODE_W && test != WV_MODE_V) return set_err(WV_EINVAL, "test must be W or V");
+    return schedule(g_sched, p, test == WV_MODE_W ? 0 : 1);
+}
+
+extern "C" uint64_t wv_launch_count(void) { return g_launches.load(); }
+
+extern "C" const char *wv_version(void) {
+    return "libwv 0.1 (sm_100a; Mont32 p<2^30, Mont64 p<2^62; sieve+plan+residue+finalize)";
+}
+
+extern "C" const char *wv_last_error(void) { return g_err; }

@@ -1,0 +1,394 @@
+// wv_residue.cuh -- plan, residue (hot loop) and finalize kernels.
+//
+// Per (prime, test) "record" k, the congruence L X == sum_j a_j S(x_j, y_j)
+// has T = sum_j #{s : x_j p < s < y_j p} terms.  The
+// T terms, concatenated sum after sum, are cut into chunks of 32*L terms;
+// a chunk is one warp's work item, each lane a contiguous run of <= L terms.
+//
+// Lane hot loop: eqnComputeS
+//     c1 <- c1 u + c0 ;  c0 <- c0 u          (u = s^e, e = 3 for W, 2 for V)
+// with both products Montgomery products, the "+ c0" folded into the first
+// REDC, and u = s^e advanced by exact finite differences (e = 3:
+// u += d1, d1 += d2, d2 += 6; e = 2: u += d1, d1 += 2) -- modular adds only,
+// so 2 Montgomery multiplies per term.  c1/c0 is then sum 1/u = S(x, y): the
+// recurrence is Montgomery's batched-inversion trick specialised to a sum of
+// inverses (one inversion per record, in finalize).
+//
+// At the end of a sum's run the lane folds the coefficient (c1 <- a_j c1) and
+// merges the run into its accumulator with eqnCombinePairs:
+//     (c0, c1) (+) (c0', c1') = (c0 c0', c0 c1' + c1 c0').
+// Lanes merge by 5 xor-shuffle rounds; lane 0 stores the chunk's pair.
+// Finalize merges a record's chunk pairs and returns
+//     X = C1 * (C0 * L)^{-1}  mod p.
+#pragma once
+#include <stdint.h>
+#include "wv_mont.cuh"
+
+namespace wv {
+
+struct Term { int64_t a; uint32_t xn, xd, yn, yd; };
+struct Cong {
+    char name[8];
+    int64_t L;
+    uint32_t e, m, min_p, excluded_p;
+    Term t[33];
+};
+
+constexpr int NCONG = 14;
+__constant__ Cong c_cong[NCONG];
+
+struct Rec {                // one (prime, test) pair; 32 bytes
+    uint64_t p;
+    uint64_t T;             // number of terms
+    uint32_t cid;           // congruence id
+    uint32_t L;             // terms per lane in a full chunk
+    uint32_t idx;           // output index of the prime
+    uint32_t test;          // 0 = W (B_{p-3}), 1 = V (E_{p-3})
+};
+
+struct Sched {              // default schedule + overrides
+    uint64_t small;         // p < small uses the one-sum forms
+    int w_small, w_big, v_small, v_big;   // congruence ids
+    int w_force, v_force;   // -1 = none
+};
+
+constexpr uint32_t CAP_CHUNKS = 1024;   // target max chunks per record
+constexpr uint32_t LMIN = 4096;         // min terms per lane in a full chunk
+constexpr uint64_t WIDTH32_MAX = 1ull << 30;  // Mont32 (lazy, fused) needs p < 2^30
+
+// ids in congruences.inc order
+enum { C_VOR12 = 0, C_BB1 = 1, C_BB2, C_BB6, C_BB9, C_BB16, C_BB22, C_BB30,
+       C_EE3, C_EE5, C_EE9, C_EE16, C_EE24, C_EE33 };
+
+__host__ __device__ __forceinline__ int schedule(const Sched &s, uint64_t p, int test) {
+    if (test == 0) {
+        if (s.w_force >= 0) return s.w_force;
+        if (p == 7) return C_VOR12;
+        return p < s.small ? s.w_small : s.w_big;
+    }
+    if (s.v_force >= 0) return s.v_force;
+    return p < s.small ? s.v_small : s.v_big;
+}
+
+// first and count of integers s with x p < s < y p  (x = xn/xd, y = yn/yd), exact.
+__device__ __forceinline__ void sum_bounds(uint64_t p, const Term &t, uint64_t *first, uint64_t *count) {
+    uint64_t qx = p / t.xd, rx = p % t.xd;
+    uint64_t fl = (uint64_t)t.xn * qx + ((uint64_t)t.xn * rx) / t.xd;      // floor(x p)
+    uint64_t qy = p / t.yd, ry = p % t.yd;
+    uint64_t ce = (uint64_t)t.yn * qy + ((uint64_t)t.yn * ry + t.yd - 1) / t.yd;  // ceil(y p)
+    uint64_t f = fl + 1, l = ce - 1;
+    *first = f;
+    *count = l >= f ? l - f + 1 : 0;
+}
+
+// ---------------------------------------------------------------- plan
+// One thread per record k = i * ntests + t (i < n_primes read from device).
+__global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ n_primes_dev,
+                            uint64_t n_primes_host, uint64_t kmax, uint32_t mode, Sched sched,
+                            Rec *__restrict__ recs, uint64_t *__restrict__ nchunks,
+                            unsigned long long *__restrict__ first64, int *__restrict__ err) {
+    const uint32_t ntests = (mode == 3) ? 2 : 1;
+    const uint64_t n = n_primes_dev ? *n_primes_dev : n_primes_host;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kmax;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = k / ntests;
+        if (i >= n) { nchunks[k] = 0; recs[k].T = 0; recs[k].p = 0; continue; }
+        const uint32_t test = (mode == 3) ? (uint32_t)(k % ntests) : (mode == 1 ? 0u : 1u);
+        const uint64_t p = primes[i];
+        const int cid = schedule(sched, p, (int)test);
+        if (cid < 0 || cid >= NCONG || p < c_cong[cid].min_p || p == c_cong[cid].excluded_p ||
+            (test == 0) != (c_cong[cid].e == 3) || p < 5 || p >= (1ull << 62)) {
+            atomicExch(err, 1);
+            nchunks[k] = 0; recs[k].T = 0; recs[k].p = 0; continue;
+        }
+        const Cong &c = c_cong[cid];
+        uint64_t T = 0;
+        for (uint32_t j = 0; j < c.m; j++) {
+            uint64_t f, cnt;
+            sum_bounds(p, c.t[j], &f, &cnt);
+            T += cnt;
+        }
+        uint64_t L = (T + 32ull * CAP_CHUNKS - 1) / (32ull * CAP_CHUNKS);
+        if (L < LMIN) L = LMIN;
+        if (L > 0x40000000ull) L = 0x40000000ull;
+        const uint64_t nc = (T + 32 * L - 1) / (32 * L);
+        Rec r;
+        r.p = p; r.T = T; r.cid = (uint32_t)cid; r.L = (uint32_t)L; r.idx = (uint32_t)i; r.test = test;
+        recs[k] = r;
+        nchunks[k] = nc;
+        if (p >= WIDTH32_MAX && nc > 0) atomicMin(first64, (unsigned long long)k);
+    }
+}
+
+// item g -> record k: the largest k in [klo, khi) with start[k] <= g
+__device__ __forceinline__ uint64_t find_rec(const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi, uint64_t g) {
+    uint64_t lo = klo, hi = khi;          // invariant: start[lo] <= g, answer in [lo, hi)
+    while (hi - lo > 1) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (start[mid] <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------- term runs
+// n terms s = s0, s0+1, ...: returns the pair for prod (z + s^e) in Montgomery form.
+template <class M, int E>
+__device__ __forceinline__ void run_terms(const M &mo, uint64_t s0, uint32_t n,
+                                          typename M::W &c0, typename M::W &c1) {
+    using W = typename M::W;
+    const W sm = mo.to(s0);
+    W u, d1, d2, d3;
+    if (E == 3) {
+        const W s2 = mo.mul(sm, sm);
+        u = mo.mul(s2, sm);
+        const W s2x3 = mo.add(mo.add(s2, s2), s2);
+        const W smx3 = mo.add(mo.add(sm, sm), sm);
+        d1 = mo.add(mo.add(s2x3, smx3), mo.r1);                  // 3s^2 + 3s + 1
+        const W smx6 = mo.add(smx3, smx3);
+        const W r1x3 = mo.add(mo.add(mo.r1, mo.r1), mo.r1);
+        const W r1x6 = mo.add(r1x3, r1x3);
+        d2 = mo.add(smx6, r1x6);                                  // 6s + 6
+        d3 = r1x6;                                                // 6
+    } else {
+        u = mo.mul(sm, sm);
+        d1 = mo.add(mo.add(sm, sm), mo.r1);                       // 2s + 1
+        d2 = mo.add(mo.r1, mo.r1);                                // 2
+        d3 = 0;
+    }
+    W a0 = mo.r1, a1 = 0;
+    uint32_t i = 0;
+    #pragma unroll 1
+    for (; i + 4 <= n; i += 4) {
+        #pragma unroll
+        for (int k = 0; k < 4; k++) {
+            a1 = mo.muladd(a1, u, a0);
+            a0 = mo.mul(a0, u);
+            u = mo.add(u, d1);
+            d1 = mo.add(d1, d2);
+            if (E == 3) d2 = mo.add(d2, d3);
+        }
+    }
+    for (; i < n; i++) {
+        a1 = mo.muladd(a1, u, a0);
+        a0 = mo.mul(a0, u);
+        u = mo.add(u, d1);
+        d1 = mo.add(d1, d2);
+        if (E == 3) d2 = mo.add(d2, d3);
+    }
+    c0 = a0; c1 = a1;
+}
+
+template <class M>
+__device__ __forceinline__ void combine(const M &mo, typename M::W &C0, typename M::W &C1,
+                                        typename M::W c0, typename M::W c1) {
+    typename M::W n1 = mo.add(mo.mul(C0, c1), mo.mul(C1, c0));
+    C0 = mo.mul(C0, c0);
+    C1 = n1;
+}
+
+constexpr int RES_THREADS = 256;
+constexpr int RES_WARPS = RES_THREADS / 32;
+
+// Persistent: each warp pulls items g in [g_lo, g_hi) from *counter (reset to 0 before launch).
+template <class M>
+__global__ void __launch_bounds__(RES_THREADS)
+residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
+               uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
+               unsigned long long *__restrict__ counter) {
+    using W = typename M::W;
+    __shared__ uint64_t s_first[RES_WARPS][34];
+    __shared__ uint64_t s_cum[RES_WARPS][35];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (;;) {
+        unsigned long long gi = 0;
+        if (lane == 0) gi = atomicAdd(counter, 1ull);
+        gi = __shfl_sync(0xffffffffu, gi, 0);
+        const uint64_t g = g_lo + gi;
+        if (g >= g_hi) break;
+        const uint64_t k = find_rec(start, klo, khi, g);
+        const Rec r = recs[k];
+        if ((r.p >= WIDTH32_MAX) != (sizeof(W) == 8)) continue;   // the other width's kernel does it
+        const uint64_t c = g - start[k];
+        const Cong &cg = c_cong[r.cid];
+        const uint32_t m = cg.m;
+        M mo;
+        mo.init(r.p);
+        for (uint32_t j = lane; j < m; j += 32) {
+            uint64_t f, cnt;
+            sum_bounds(r.p, cg.t[j], &f, &cnt);
+            s_first[wid][j] = f;
+            s_cum[wid][j + 1] = cnt;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            uint64_t acc = 0;
+            s_cum[wid][0] = 0;
+            for (uint32_t j = 0; j < m; j++) { acc += s_cum[wid][j + 1]; s_cum[wid][j + 1] = acc; }
+        }
+        __syncwarp();
+        const uint64_t CT = 32ull * r.L;
+        const uint64_t base = c * CT;
+        const uint64_t nck = (r.T - base) < CT ? (r.T - base) : CT;
+        const uint64_t per = (nck + 31) >> 5;
+        uint64_t t0 = base + lane * per;
+        uint64_t t1 = t0 + per;
+        const uint64_t tend = base + nck;
+        if (t1 > tend) t1 = tend;
+        W C0 = mo.r1, C1 = 0;
+        uint32_t j = 0;
+        while (t0 < t1) {
+            while (s_cum[wid][j + 1] <= t0) j++;
+            const uint64_t se = s_cum[wid][j + 1];
+            const uint32_t n = (uint32_t)((t1 < se ? t1 : se) - t0);
+            const uint64_t s0 = s_first[wid][j] + (t0 - s_cum[wid][j]);
+            W c0, c1;
+            if (cg.e == 3) run_terms<M, 3>(mo, s0, n, c0, c1);
+            else run_terms<M, 2>(mo, s0, n, c0, c1);
+            c1 = mo.mul(c1, mo.to(smod(cg.t[j].a, r.p)));      // fold a_j
+            combine(mo, C0, C1, c0, c1);
+            t0 += n;
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            W o0 = __shfl_xor_sync(0xffffffffu, C0, o);
+            W o1 = __shfl_xor_sync(0xffffffffu, C1, o);
+            combine(mo, C0, C1, o0, o1);
+        }
+        if (lane == 0) partials[g - part_base] = make_ulonglong2((unsigned long long)C0, (unsigned long long)C1);
+        __syncwarp();
+    }
+}
+
+// One warp per record in [klo, khi): merge the record's chunk pairs, invert, store.
+template <class M>
+__device__ __forceinline__ void finalize_one(const Rec &r, const uint64_t *start, uint64_t k, uint64_t part_base,
+                                             const ulonglong2 *partials, uint64_t *res_w, uint64_t *res_v) {
+    using W = typename M::W;
+    const int lane = threadIdx.x & 31;
+    M mo;
+    mo.init(r.p);
+    W C0 = mo.r1, C1 = 0;
+    const uint64_t s = start[k], e = start[k + 1];
+    for (uint64_t g = s + lane; g < e; g += 32) {
+        ulonglong2 v = partials[g - part_base];
+        combine(mo, C0, C1, (W)v.x, (W)v.y);
+    }
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        W o0 = __shfl_xor_sync(0xffffffffu, C0, o);
+        W o1 = __shfl_xor_sync(0xffffffffu, C1, o);
+        combine(mo, C0, C1, o0, o1);
+    }
+    if (lane == 0) {
+        const Cong &cg = c_cong[r.cid];
+        const W Lm = mo.to(smod(cg.L, r.p));
+        const W den = mo.mul(C0, Lm);
+        const W X = mo.mul(C1, mont_inv(mo, den));
+        const uint64_t x = mo.canon(X);
+        if (r.test == 0) res_w[r.idx] = x; else res_v[r.idx] = x;
+    }
+}
+
+__global__ void finalize_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
+                                uint64_t klo, uint64_t khi, uint64_t part_base,
+                                const ulonglong2 *__restrict__ partials,
+                                uint64_t *__restrict__ res_w, uint64_t *__restrict__ res_v) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = klo + warp; k < khi; k += nwarps) {
+        const Rec r = recs[k];
+        if (r.p == 0) continue;                     // padding record (beyond n primes)
+        if (r.p < WIDTH32_MAX) finalize_one<Mont32>(r, start, k, part_base, partials, res_w, res_v);
+        else finalize_one<Mont64>(r, start, k, part_base, partials, res_w, res_v);
+    }
+}
+
+// ---------------------------------------------------------------- checksum / hits
+__host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {   // splitmix64 finaliser
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t checksum_term(uint64_t p, uint64_t rw, uint64_t rv) {
+    return mix64(p ^ rotl64(rw, 21) ^ rotl64(rv, 42));
+}
+
+__global__ void flags_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ n_dev,
+                             uint64_t n_host, uint64_t kmax, uint64_t *__restrict__ res_w,
+                             uint64_t *__restrict__ res_v, uint32_t mode, uint32_t *__restrict__ flags,
+                             unsigned long long *__restrict__ checksum) {
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    uint64_t acc = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < kmax;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t f = 0;
+        if (i < n) {
+            uint64_t rw = ~0ull, rv = ~0ull;
+            if (mode & 1) rw = res_w[i]; else res_w[i] = ~0ull;
+            if (mode & 2) rv = res_v[i]; else res_v[i] = ~0ull;
+            f = (rw == 0 ? 1u : 0u) | (rv == 0 ? 2u : 0u);
+            acc += checksum_term(primes[i], rw, rv);
+        }
+        if (flags) flags[i] = f ? 1u : 0u;
+    }
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && checksum) atomicAdd(checksum, (unsigned long long)acc);
+}
+
+struct HitOut { uint64_t p; uint32_t flags; uint32_t reserved; };
+
+__global__ void hits_scatter_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ n_dev,
+                                    uint64_t kmax, const uint64_t *__restrict__ res_w,
+                                    const uint64_t *__restrict__ res_v, const uint32_t *__restrict__ flags,
+                                    const uint64_t *__restrict__ pos, HitOut *__restrict__ hits) {
+    const uint64_t n = *n_dev;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < kmax && i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!flags[i]) continue;
+        HitOut h;
+        h.p = primes[i];
+        h.flags = (res_w[i] == 0 ? 1u : 0u) | (res_v[i] == 0 ? 2u : 0u);
+        h.reserved = 0;
+        hits[pos[i]] = h;
+    }
+}
+
+struct ResOut { uint64_t p, rw, rv; };
+__global__ void pack_residues_kernel(const uint64_t *__restrict__ primes, uint64_t n,
+                                     const uint64_t *__restrict__ res_w, const uint64_t *__restrict__ res_v,
+                                     ResOut *__restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = ResOut{primes[i], res_w[i], res_v[i]};
+}
+
+// first item of the first 64-bit record, and the batch boundaries
+__global__ void split_kernel(const uint64_t *__restrict__ start, uint64_t K, const unsigned long long *first64,
+                             uint64_t *__restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned long long k = *first64;
+        out[0] = (k >= K) ? start[K] : start[k];   // start has K+1 entries (start[K] = total)
+        out[1] = (k >= K) ? K : k;
+    }
+}
+
+// For batch b (1 <= b < nb): record index kb[b] = largest k with start[k] <= b * step (k in [0, K]);
+// kb[nb + 1 + b] = start[kb[b]] (the batch's first item).
+__global__ void batch_bounds_kernel(const uint64_t *__restrict__ start, uint64_t K, uint64_t step, uint64_t nb,
+                                    uint64_t *__restrict__ kb) {
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (uint64_t)gridDim.x * blockDim.x) {
+        if (b == 0) { kb[0] = 0; kb[nb + 1] = 0; continue; }
+        if (b == nb) { kb[b] = K; kb[nb + 1 + b] = start[K]; continue; }
+        const uint64_t target = b * step;
+        uint64_t lo = 0, hi = K + 1;
+        while (hi - lo > 1) {
+            uint64_t mid = (lo + hi) >> 1;
+            if (start[mid] <= target) lo = mid; else hi = mid;
+        }
+        kb[b] = lo;
+        kb[nb + 1 + b] = start[lo];
+    }
+}
+
+}  // namespace wv

@@ -1,0 +1,22 @@
+"""Scratch timing of wv_search_device on BASELINE windows (CUDA events; not a bench line)."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2101_11157_b200 as wv
+from paper_2101_11157_b200.workloads import CONFIGS, SUBWINDOWS
+
+names = sys.argv[1:] or ["c1", "c2"]
+for name in names:
+    w = CONFIGS.get(name) or SUBWINDOWS[name]
+    ds = wv.DeviceSearch(w.lo, w.hi, w.mode)
+    ds.run()
+    reps = 3 if name in ("c1", "c2") else 1
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        ds.run()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    print(f"{name}: {ds.n_primes} primes, {ds.n_hits} hits, {ms:.3f} ms/run, {ds.n_primes / ms * 1e3:.1f} primes/s", flush=True)

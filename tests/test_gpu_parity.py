@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the paper.
+
+Bit-exact comparison of canonical residues (integer work: the bar is equality).
+Inputs are the BASELINE configs (paper_2101_11157_b200.workloads) and seeded
+random windows; expected values come from oracle/ (on the fly for small
+windows, or tests/golden/oracle_*.npz written by scripts/gen_oracle_goldens.py)
+and from the paper's printed tables (tests/golden/paper_*).
+"""
+import csv
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2101_11157_b200.workloads import CONFIGS, SUBWINDOWS, random_windows, sample_indices
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+NONE = (1 << 64) - 1
+
+
+def _golden(name):
+    path = os.path.join(GOLD, f"oracle_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated (scripts/gen_oracle_goldens.py {name})")
+    z = np.load(path)
+    return z["p"], z["res_w"], z["res_v"], json.loads(str(z["meta"]))
+
+
+def _table(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return list(csv.DictReader(r for r in f if not r.startswith("#")))
+
+
+def _oracle_arrays(ps, mode):
+    out = oracle.residues(ps, mode)
+    rw = np.array([NONE if r[1] is None else r[1] for r in out], dtype=np.uint64)
+    rv = np.array([NONE if r[2] is None else r[2] for r in out], dtype=np.uint64)
+    return rw, rv
+
+
+def _assert_equal(p, got, want, what):
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, f"{what}: {bad.size} mismatches, first p={p[bad[:5]].tolist()} " \
+                          f"got={got[bad[:5]].tolist()} want={want[bad[:5]].tolist()}"
+
+
+# ---------------------------------------------------------------- whole windows
+def test_c1_full_bit_exact(wv):
+    """configs[0]: every prime 5 <= p < 10^5, both tests, vs oracle goldens; hits recovered."""
+    w = CONFIGS["c1"]
+    hits, res = wv.search(w.lo, w.hi, w.mode)
+    gp, gw, gv, meta = _golden("c1")
+    assert res["p"].tolist() == gp.tolist()
+    _assert_equal(gp, res["res_w"], gw, "W")
+    _assert_equal(gp, res["res_v"], gv, "V")
+    assert {(int(h["p"]), int(h["flags"])) for h in hits} == {(149, 2), (241, 2), (16843, 1)}
+
+
+def test_c2_full_bit_exact(wv):
+    """configs[1]: every prime p < 3*10^6, both tests, through the device API bench.py times."""
+    w = CONFIGS["c2"]
+    gp, gw, gv, meta = _golden("c2")
+    ds = wv.DeviceSearch(w.lo, w.hi, w.mode).run()
+    p = ds.primes_np()
+    assert p.tolist() == gp.tolist()
+    rw, rv = ds.res_np()
+    _assert_equal(gp, rw, gw, "W")
+    _assert_equal(gp, rv, gv, "V")
+    hits = {(int(h["p"]), int(h["flags"])) for h in ds.hits_np()}
+    assert hits == {(149, 2), (241, 2), (16843, 1), (2124679, 1), (2946901, 2)}
+    want_chk = sum(wv.checksum_term(int(a), int(b), int(c)) for a, b, c in zip(gp, gw, gv)) % (1 << 64)
+    assert ds.checksum_int() == want_chk
+
+
+def test_random_windows_vs_oracle(wv):
+    """Seeded ragged windows (several sieve segments and residue chunks, odd tails)."""
+    for i, (a, b) in enumerate(random_windows(2101, 6, 5, 4 * 10 ** 6, 1, 300000)):
+        mode = 1 + i % 3
+        hits, res = wv.search(a, b, mode)
+        ps = oracle.primes(max(a, 5), b)
+        assert res["p"].tolist() == ps, (a, b)
+        rw, rv = _oracle_arrays(ps, mode)
+        p = np.array(ps, dtype=np.uint64)
+        _assert_equal(p, res["res_w"], rw, f"W [{a},{b})")
+        _assert_equal(p, res["res_v"], rv, f"V [{a},{b})")
+
+
+def test_c3_full_window_sampled(wv):
+    """configs[2] at full size ([1.0e9, 1.05e9), V): 64 sampled primes vs oracle goldens,
+    no Vandiver prime (reading R4) and no |<E>| < 50 (Table 3 is complete)."""
+    w = CONFIGS["c3"]
+    gp, gw, gv, meta = _golden("c3")
+    ds = wv.DeviceSearch(w.lo, w.hi, w.mode).run()
+    p = ds.primes_np()
+    assert len(p) == meta["primes_in_window"] == 2409816
+    idx = sample_indices(len(p), 64)
+    assert p[idx].tolist() == gp.tolist()
+    rw, rv = ds.res_np()
+    _assert_equal(gp, rv[idx], gv, "V sample")
+    assert (rw == NONE).all()
+    assert ds.n_hits == 0
+    sym = np.where(rv > (p - 1) // 2, rv.astype(np.int64) - p.astype(np.int64), rv.astype(np.int64))
+    assert int((np.abs(sym) < 50).sum()) == 0
+
+
+def test_pin_window_recovers_1062232319(wv):
+    w = CONFIGS["pin_v"]
+    gp, gw, gv, meta = _golden("pin_v")
+    hits, res = wv.search(w.lo, w.hi, w.mode)
+    assert [(int(h["p"]), int(h["flags"])) for h in hits] == [(1062232319, 2)]
+    d = dict(zip(res["p"].tolist(), res["res_v"].tolist()))
+    assert [d[int(x)] for x in gp] == gv.tolist()
+
+
+# ---------------------------------------------------------------- paper-printed values
+def _sym(r, p):
+    return r - p if r > (p - 1) // 2 else r
+
+
+def test_table2_all_rows(wv):
+    """Table 2: all 19 near misses of B_{p-3} in (1e9, 6e10), sign-exact (64-bit path)."""
+    rows = _table("paper_table2_bernoulli.csv")
+    ps = [int(r["p"]) for r in rows]
+    rw, rv = wv.residues_of(ps, wv.MODE_W)
+    for r, x in zip(rows, rw.tolist()):
+        assert _sym(int(x), int(r["p"])) == int(r["symres_B"]), r
+
+
+def test_table3_all_rows(wv):
+    """Table 3: 11 rows exact, 7 rows |value| with the secant sign (reading R2)."""
+    rows = _table("paper_table3_euler.csv")
+    ps = [int(r["p"]) for r in rows]
+    rw, rv = wv.residues_of(ps, wv.MODE_V)
+    for r, x in zip(rows, rv.tolist()):
+        v, want = _sym(int(x), int(r["p"])), int(r["symres_E"])
+        if int(r["sign_exact"]):
+            assert v == want, r
+        else:
+            assert v == -want and want != 0, r
+
+
+def test_known_primes(wv):
+    k = json.load(open(os.path.join(GOLD, "paper_known_primes.json")))
+    ps = k["wolstenholme_below_6e10"] + k["vandiver_below_4e10"]
+    rw, rv = wv.residues_of(ps, wv.MODE_BOTH)
+    for p, a, b in zip(ps, rw.tolist(), rv.tolist()):
+        assert (a == 0) == (p in k["wolstenholme_below_6e10"]), p
+        assert (b == 0) == (p in k["vandiver_below_4e10"]), p
+    rw, rv = wv.residues_of([2124679], wv.MODE_V)
+    assert _sym(int(rv[0]), 2124679) == -85724         # reading R3
+
+
+def test_sieve_counts_match_paper(wv):
+    """The device sieve reproduces the paper's prime counts and textbook pi(x)."""
+    counts = json.load(open(os.path.join(GOLD, "paper_prime_counts.json")))["counts"]
+    for c in counts:
+        assert wv.prime_count(max(c["lo"], 5), c["hi"]) == c["n"] - (2 if c["lo"] < 5 and c["hi"] > 3 else 0), c
+
+
+# ---------------------------------------------------------------- cross-congruence / schedule
+def test_every_congruence_on_gpu(wv):
+    """Force each congruence (VOR12 at p >= 7) on a mixed-width unsorted list vs the oracle/paper."""
+    rng = np.random.default_rng(5)
+    small = oracle.primes(11, 30000)
+    ps = sorted(set(rng.choice(small, 40, replace=False).tolist()) | {11, 13, 29989})
+    big_w = [1025793739, 2139716869, 56604583391]       # Table 2
+    big_v = [1062232319, 1836806681, 36652898767]       # Table 3 (sign-exact rows)
+    names = {c["name"]: c["id"] for c in wv.congruences()}
+    try:
+        for name, cid in names.items():
+            e3 = name.startswith("BB") or name == "VOR12"
+            wv.set_schedule_override(cid if e3 else -1, -1 if e3 else cid)
+            lst = ps + (big_w if e3 else big_v)
+            rng.shuffle(lst)
+            rw, rv = wv.residues_of(lst, wv.MODE_W if e3 else wv.MODE_V)
+            got = rw if e3 else rv
+            for p, x in zip(lst, got.tolist()):
+                want = (oracle.residue_B(p) if p < 10 ** 8 else None) if e3 else \
+                       (oracle.residue_E(p) if p < 10 ** 8 else None)
+                if want is None:
+                    tab = {1025793739: -9, 2139716869: 2, 56604583391: -25, 1062232319: 0,
+                           1836806681: -15, 36652898767: -9}
+                    assert _sym(int(x), p) == tab[p], (name, p)
+                else:
+                    assert int(x) == want, (name, p)
+    finally:
+        wv.set_schedule_override(-1, -1)
+
+
+# ---------------------------------------------------------------- sharding / edge cases
+def test_shards_union_equals_whole(wv):
+    """Interleaved blocks: union of shards == unsharded; checksums add up."""
+    lo, hi = 1000, 1000 + 40 * 131072 + 777
+    _, whole, chk = wv.search_shard(lo, hi, 3, 0, 1, 0)
+    for nsh in (2, 3, 8):
+        parts, tot = [], 0
+        for s in range(nsh):
+            _, r, c = wv.search_shard(lo, hi, 3, s, nsh, 131072)
+            parts.append(r)
+            tot = (tot + c) % (1 << 64)
+        merged = np.sort(np.concatenate(parts), order="p")
+        assert merged.tobytes() == whole.tobytes()
+        assert tot == chk
+
+
+def test_edge_windows(wv):
+    h, r = wv.search(100, 101, 3)
+    assert len(r) == 0 and len(h) == 0
+    h, r = wv.search(0, 5, 3)
+    assert len(r) == 0
+    h, r = wv.search(5, 6, 3)
+    assert r.tolist() == [(5, 1, 1)]
+    h, r = wv.search(7, 8, 3)
+    assert r.tolist() == [(7, 3, 5)]                      # B_4 = -1/30 == 3, E_4 = 5 (mod 7)
+    h, r = wv.search(5, 12, 1)
+    assert r["res_v"].tolist() == [NONE] * 3 and r["res_w"].tolist() == [1, 3, 4]
+    for bad in [(10, 10, 3), (10, 5, 3), (5, 100, 0), (5, 100, 4), (5, (1 << 62) + 1, 3)]:
+        with pytest.raises(wv.WVError):
+            wv.search(*bad)
+    with pytest.raises(wv.WVError):
+        wv.search_shard(5, 100, 3, 2, 2, 0)
+
+
+def test_ragged_tail_64bit_window(wv):
+    """A small window just above 2^30 (first 64-bit primes) and one at 5.9e10 (C4 head), vs oracle."""
+    a, b = (1 << 30) - 3000, (1 << 30) + 3000
+    hits, res = wv.search(a, b, 3)
+    ps = oracle.primes(a, b)
+    assert res["p"].tolist() == ps
+    for r in res[sample_indices(len(res), 4)]:
+        p = int(r["p"])
+        assert int(r["res_w"]) == oracle.B_stafford_vandiver(p), p   # tier C (pinned in test_oracle_pins)
+        assert int(r["res_v"]) == oracle.E_quarter(p), p
+    w = SUBWINDOWS["c4_head"]
+    hits, res = wv.search(w.lo, w.hi, w.mode)
+    assert res["p"].tolist() == oracle.primes(w.lo, w.hi)
