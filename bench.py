@@ -1,0 +1,324 @@
+#!/usr/bin/env python3
+"""bench.py -- primes tested per second (W+V) on B200, per the driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path (sieve -> plan ->
+residue -> finalize -> hits/checksum) over one BASELINE window.  The default
+workload is configs[1] = C2: every prime p < 3*10^6, both tests (the config the
+metric is quoted on that fits one GPU).  With N GPUs
+(torchrun) the window is split into interleaved blocks (rank r takes blocks
+b == r mod N; strong scaling: total work fixed) and the per-rank hit lists and
+checksums are gathered with NCCL (the only collective the path has).
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events
+on the launching stream, with a 256 MiB L2-flush write between steps (outside
+the events); barrier + synchronize around the timed region; the max over ranks
+is reported.  nvidia-smi is sampled during the timed region.
+
+`value`  -- device-resident path (wv_search_device into torch buffers).
+`e2e`    -- the host-buffer public API (wv_search_shard): results copied D2H
+            into host memory every step, wall clock, max over ranks.
+`roofline` -- the dominant kernel (residue_kernel) via the library's CUDA-event
+            stats hook: algorithmic Montgomery multiplications / its device time,
+            against the IMAD-pipe peak.
+`cpu_baseline` -- the CPU oracle (oracle/) as it stands, on a bounded sample
+            of the same workload, on this box's host cores (rank 0, N=1 only).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "primes tested/sec (W+V)"
+UNIT = "primes/s"
+
+# Montgomery multiplications per term: c1 <- c1 u + c0, c0 <- c0 u
+MULMODS_PER_TERM = 2
+# 32-bit multiplies (IMAD-class) per Montgomery product: Mont32 = 3 (a*b wide, m = lo*p', hi(m*p));
+# Mont64 = 11 (4 partial products for a*b, 3 for lo64(lo*p'), 4 for hi(m*p)).  DESIGN.md "Roofline".
+IMUL_PER_MULMOD = {32: 3, 64: 11}
+IMAD_PER_CLK_PER_SM = 64      # FMA-heavy pipe: 16 lanes/clk/SMSP x 4 SMSP (B300_MICROARCH.md "Pipe rates")
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = set(gpus)
+        self.proc = None
+        self.path = f"/tmp/wv_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                if int(parts[0]) not in self.gpus:
+                    continue
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def _window(name):
+    from paper_2101_11157_b200.workloads import CONFIGS, SUBWINDOWS
+    w = CONFIGS.get(name) or SUBWINDOWS.get(name)
+    if w is None:
+        raise SystemExit(f"unknown workload {name}")
+    return w
+
+
+def cpu_oracle_rate(w, sample_k, workers):
+    """Oracle primes/s on a deterministic sample of the window's primes (all host cores)."""
+    import oracle
+    from paper_2101_11157_b200.workloads import sample_indices
+    ps = oracle.primes(max(w.lo, 5), w.hi)
+    sample = [ps[i] for i in sample_indices(len(ps), sample_k)]
+    t0 = time.perf_counter()
+    oracle.residues(sample, w.mode, workers=workers)
+    dt = time.perf_counter() - t0
+    return len(sample) / dt, dt, len(sample), len(ps)
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on the same workload (rank 0 only)."""
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    w = _window(args.workload)
+    cores = os.cpu_count() or 1
+    k = max(1, args.ref_sample // 2)
+    times = []
+    for i in range(args.warmup + args.steps):
+        rate, dt, n, n_all = cpu_oracle_rate(w, k, cores)
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = k / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": w.name, "window": [w.lo, w.hi], "mode": "W+V" if w.mode == 3 else "WV"[w.mode - 1],
+                       "step": f"oracle residues of a {k}-prime deterministic sample (floor(j*N/k)) of the window"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{k} of {n_all} primes of {w.name}, one prime per task"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=2048, help="primes in the oracle's bounded sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2101_11157_b200 as wv
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = _window(args.workload)
+    ds = wv.DeviceSearch(w.lo, w.hi, w.mode, shard=rank, nshards=world, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def gather(ds):
+        """NCCL all_gather of per-rank (n_primes, n_hits, checksum) and the hit lists."""
+        meta = torch.tensor([ds.n_primes, ds.n_hits, 0], dtype=torch.int64, device=dev)
+        meta[2:3].copy_(ds.checksum)
+        allm = [torch.empty_like(meta) for _ in range(world)]
+        dist.all_gather(allm, meta)
+        mh = max(int(m[1]) for m in allm)
+        hits = torch.zeros(2 * max(mh, 1), dtype=torch.int64, device=dev)
+        hits[: 2 * ds.n_hits].copy_(ds.hits[: 2 * ds.n_hits])
+        allh = [torch.empty_like(hits) for _ in range(world)]
+        dist.all_gather(allh, hits)
+        return allm, allh
+
+    def step():
+        ds.run(stream)
+        if world > 1:
+            return gather(ds)
+        return None
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    wv.stats_reset()
+    wv.stats_enable(True)
+    launches0 = wv.launch_count()
+    clocks = ClockSampler(range(world) if rank == 0 else [])
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if rank == 0:
+        clocks.start()
+    evs = []
+    for _ in range(args.steps):
+        flush.fill_(1)                                  # L2 flush between steps (outside the events)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if rank == 0 else None
+    wv.stats_enable(False)
+    st = wv.stats()
+    launches = wv.launch_count() - launches0           # our kernels inside the timed region
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n_tot = torch.tensor([ds.n_primes], dtype=torch.int64, device=dev)
+        dist.all_reduce(n_tot)
+        n_all = int(n_tot.item())
+    else:
+        n_all = ds.n_primes
+    ms_max = float(t.item())
+    value = n_all / (ms_max / 1e3)
+
+    # e2e through the host-buffer API (results D2H every step), wall clock, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(2):
+            wv.search_shard(w.lo, w.hi, w.mode, rank, world, 0)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            hits_h, res_h, chk = wv.search_shard(w.lo, w.hi, w.mode, rank, world, 0)
+        dt = (time.perf_counter() - t0) / args.steps
+        te = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        d2h = int(res_h.nbytes + hits_h.nbytes + 8)
+        e2e = {"value": n_all / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * float(te.item()),
+               "api": "wv_search_shard (host buffers; inputs are the window bounds passed by value)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel: residue_kernel (Mont32 for C1-C3 windows, Mont64 above 2^30)
+    peaks, peak_kind = _peaks()
+    steps = args.steps
+    terms = st["terms"] / steps
+    terms32 = st["terms32"] / steps
+    res_ms = st["residue_ms"] / steps
+    res32_ms = st["residue32_ms"] / steps
+    width = 32 if terms32 >= terms - terms32 else 64
+    k_terms = terms32 if width == 32 else terms - terms32
+    k_ms = res32_ms if width == 32 else res_ms - res32_ms
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_imul = IMAD_PER_CLK_PER_SM * sms * mhz * 1e6
+    peak_mulmod = peak_imul / IMUL_PER_MULMOD[width]
+    achieved = MULMODS_PER_TERM * k_terms / (k_ms / 1e3) if k_ms > 0 else 0.0
+    roof = {"bound": "alu", "kernel": f"residue_kernel<Mont{width}>", "achieved": achieved / 1e9,
+            "peak": peak_mulmod / 1e9, "unit": "Gmulmod/s", "frac": achieved / peak_mulmod if peak_mulmod else None,
+            "traffic": None,
+            "peak_basis": f"{IMAD_PER_CLK_PER_SM} IMAD/clk/SM x {sms} SMs x {mhz:.0f} MHz ({peak_kind} sm_max_mhz) "
+                          f"/ {IMUL_PER_MULMOD[width]} IMAD per Mont{width} product",
+            "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms_max if ms_max else None,
+            "terms_per_step": terms, "terms_per_s": k_terms / (k_ms / 1e3) if k_ms > 0 else None}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rate, dt, n, n_all_w = cpu_oracle_rate(w, args.ref_sample, os.cpu_count() or 1)
+        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "oracle",
+               "sample": f"{n} of {n_all_w} primes of {w.name} (floor(j*N/k) sample), both tests, "
+                         f"one prime per task, {dt:.1f} s wall"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32" if width == 32 else "u64", "data": "synthetic",
+            "config": {"workload": w.name, "window": [w.lo, w.hi], "mode": {1: "W", 2: "V", 3: "W+V"}[w.mode],
+                       "primes": n_all, "parallelism": f"interleaved blocks x{world}",
+                       "l2_flush": "256 MiB write between timed steps (outside the CUDA events)",
+                       "terms_per_step": terms, "mulmods_per_s": MULMODS_PER_TERM * terms / (ms_max / 1e3)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -174,6 +174,26 @@ int wv_set_schedule_override(int w_id, int v_id);
  *                   V: p < 4096 EE3, p >= 4096 EE33.  Returns the id used. */
 int wv_schedule(uint64_t p, uint32_t test /* WV_MODE_W or WV_MODE_V */);
 
+/* Measurement hooks (process-wide, for bench.py / profiling).  When enabled,
+ * every residue-kernel launch is bracketed by CUDA events on its stream and
+ * the elapsed times are accumulated at the call's final synchronisation.
+ *   terms      algorithmic terms evaluated (sum over (prime,test) of the
+ *              congruence's term count);
+ *   residue_ms summed device time of residue-kernel launches;
+ *   residue_launches, records ((prime,test) pairs), chunks (warp work items). */
+typedef struct {
+    uint64_t terms;
+    uint64_t terms32;          /* of which in the 32-bit (p < 2^30) kernel */
+    uint64_t residue_launches;
+    uint64_t records;
+    uint64_t chunks;
+    double   residue_ms;
+    double   residue32_ms;
+} wv_stats;
+int wv_stats_enable(int on);
+int wv_stats_get(wv_stats *out);
+int wv_stats_reset(void);
+
 /* Counters: kernels launched by this library since load (process-wide). */
 uint64_t wv_launch_count(void);
 /* Library / device info string (build flags, sm, ...). */

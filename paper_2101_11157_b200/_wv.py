@@ -41,6 +41,12 @@ class _Cong(ctypes.Structure):
                 ("t", _Term * 33)]
 
 
+class Stats(ctypes.Structure):
+    _fields_ = [("terms", ctypes.c_uint64), ("terms32", ctypes.c_uint64), ("residue_launches", ctypes.c_uint64),
+                ("records", ctypes.c_uint64), ("chunks", ctypes.c_uint64), ("residue_ms", ctypes.c_double),
+                ("residue32_ms", ctypes.c_double)]
+
+
 # (name, restype, argtypes) for every symbol include/wv.h declares
 _u64, _u32, _sz, _vp, _i = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int
 _P = ctypes.POINTER
@@ -59,6 +65,9 @@ SIGNATURES = {
     "wv_congruence_get": (_i, [_i, _P(_Cong)]),
     "wv_set_schedule_override": (_i, [_i, _i]),
     "wv_schedule": (_i, [_u64, _u32]),
+    "wv_stats_enable": (_i, [_i]),
+    "wv_stats_get": (_i, [_P(Stats)]),
+    "wv_stats_reset": (_i, []),
     "wv_launch_count": (_u64, []),
     "wv_version": (ctypes.c_char_p, []),
     "wv_last_error": (ctypes.c_char_p, []),
@@ -237,6 +246,20 @@ def set_schedule_override(w_id=-1, v_id=-1):
 
 def schedule(p, test):
     return int(lib().wv_schedule(p, test))
+
+
+def stats_enable(on=True):
+    _check(lib().wv_stats_enable(1 if on else 0))
+
+
+def stats_reset():
+    _check(lib().wv_stats_reset())
+
+
+def stats():
+    s = Stats()
+    _check(lib().wv_stats_get(ctypes.byref(s)))
+    return {k: getattr(s, k) for k, _ in Stats._fields_}
 
 
 def launch_count():

@@ -42,6 +42,12 @@ static thread_local char g_err[1024] = "";
 static std::atomic<uint64_t> g_launches{0};
 static Sched g_sched = {4096, C_BB1, C_BB30, C_EE3, C_EE33, -1, -1};
 
+// measurement hooks
+static std::atomic<int> g_stats_on{0};
+static std::mutex g_stats_mu;
+static wv_stats g_stats;
+struct EvPair { cudaEvent_t a, b; bool is32; };
+
 static int set_err(int code, const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
@@ -161,7 +167,7 @@ static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 static const uint64_t PART_BUDGET = 1ull << 24;   // partial pairs per batch (256 MiB)
 
 enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2, M_CNT32 = 3, M_CNT64 = 4, M_NHITS = 5, M_CHECKSUM = 6,
-       M_NBASE1 = 7, M_SPLIT = 8 /* 2 slots */, M_SLOTS = 16 };
+       M_NBASE1 = 7, M_SPLIT = 8 /* 2 slots */, M_TERMS = 10 /* 2 slots: 32-bit, 64-bit */, M_SLOTS = 16 };
 
 struct Layout {
     // problem
@@ -317,12 +323,14 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     const unsigned grid_plan = (unsigned)((K + 255) / 256 < (uint64_t)c->sms * 32 ? (K + 255) / 256 : c->sms * 32);
     if (K > 0) {
         LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs, nch,
-               (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR));
+               (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
+               (unsigned long long *)(misc + M_TERMS));
     }
     TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
     LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, (split g32, k64)
-    uint64_t hs[2];
+    uint64_t hs[2], ht[2];
+    CK(cudaMemcpyAsync(ht, misc + M_TERMS, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 16, cudaMemcpyDeviceToHost, st));
@@ -331,6 +339,15 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     if (n_primes_out) *n_primes_out = n;
     if ((int)h[1] != 0) return set_err(WV_EINVAL, "schedule chose a congruence not valid for some prime");
     const uint64_t G = h[2];
+    const bool stats = g_stats_on.load() != 0;
+    std::vector<EvPair> evs;
+    if (stats) {
+        std::lock_guard<std::mutex> lk(g_stats_mu);
+        g_stats.terms += ht[0] + ht[1];
+        g_stats.terms32 += ht[0];
+        g_stats.records += K;
+        g_stats.chunks += G;
+    }
     uint64_t g32 = sorted ? hs[0] : G, k64 = sorted ? hs[1] : K;   // unsorted: both kernels see everything
     // batches of <= PART_BUDGET partial pairs, cut at record boundaries
     std::vector<uint64_t> hk, hg;
@@ -357,19 +374,41 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         if (b32 > a32) {
             CK(cudaMemsetAsync(misc + M_CNT32, 0, 8, st));
             const uint64_t khi32 = sorted ? (khi < k64 ? khi : k64) : khi;
+            EvPair ev{nullptr, nullptr, true};
+            if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
             LAUNCH(residue_kernel<Mont32>, c->sms * c->occ32, RES_THREADS, st, recs, start, klo,
                    khi32 > klo ? khi32 : klo + 1, a32, b32, glo, part, (unsigned long long *)(misc + M_CNT32));
+            if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         if (b64 > a64) {
             CK(cudaMemsetAsync(misc + M_CNT64, 0, 8, st));
             const uint64_t klo64 = sorted ? (klo > k64 ? klo : k64) : klo;
+            EvPair ev{nullptr, nullptr, false};
+            if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
             LAUNCH(residue_kernel<Mont64>, c->sms * c->occ64, RES_THREADS, st, recs, start, klo64, khi, a64, b64,
                    glo, part, (unsigned long long *)(misc + M_CNT64));
+            if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         const uint64_t nrec = khi - klo;
         uint64_t fb = (nrec * 32 + 255) / 256;
         if (fb > (uint64_t)c->sms * 16) fb = (uint64_t)c->sms * 16;
         LAUNCH(finalize_kernel, (unsigned)fb, 256, st, recs, start, klo, khi, glo, part, res_w, res_v);
+    }
+    if (stats && !evs.empty()) {
+        CK(cudaStreamSynchronize(st));
+        double ms = 0, ms32 = 0;
+        for (auto &e : evs) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, e.a, e.b));
+            ms += t;
+            if (e.is32) ms32 += t;
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        std::lock_guard<std::mutex> lk(g_stats_mu);
+        g_stats.residue_ms += ms;
+        g_stats.residue32_ms += ms32;
+        g_stats.residue_launches += evs.size();
     }
     return WV_OK;
 }
@@ -676,6 +715,22 @@ extern "C" int wv_schedule(uint64_t p, uint32_t test) {
 }
 
 extern "C" uint64_t wv_launch_count(void) { return g_launches.load(); }
+
+extern "C" int wv_stats_enable(int on) {
+    g_stats_on.store(on ? 1 : 0);
+    return WV_OK;
+}
+extern "C" int wv_stats_get(wv_stats *out) {
+    if (!out) return set_err(WV_EINVAL, "null");
+    std::lock_guard<std::mutex> lk(g_stats_mu);
+    *out = g_stats;
+    return WV_OK;
+}
+extern "C" int wv_stats_reset(void) {
+    std::lock_guard<std::mutex> lk(g_stats_mu);
+    memset(&g_stats, 0, sizeof g_stats);
+    return WV_OK;
+}
 
 extern "C" const char *wv_version(void) {
     return "libwv 0.1 (sm_100a; Mont32 p<2^30, Mont64 p<2^62; sieve+plan+residue+finalize)";

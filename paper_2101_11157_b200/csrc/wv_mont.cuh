@@ -91,11 +91,11 @@ struct Mont64 {
     }
 };
 
-// signed integer -> residue in [0, p)
+// signed integer -> residue in [0, p)   (no division when |a| < p)
 __device__ __forceinline__ uint64_t smod(int64_t a, uint64_t p) {
-    if (a >= 0) return (uint64_t)a % p;
-    uint64_t r = (uint64_t)(-a) % p;
-    return r ? p - r : 0;
+    uint64_t m = a >= 0 ? (uint64_t)a : (uint64_t)(-a);
+    if (m >= p) m %= p;
+    return a >= 0 ? m : (m ? p - m : 0);
 }
 
 // x^(p-2) in Montgomery form (Fermat inverse of a unit x, lazy in / lazy out)

@@ -86,13 +86,14 @@ __device__ __forceinline__ void sum_bounds(uint64_t p, const Term &t, uint64_t *
 __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ n_primes_dev,
                             uint64_t n_primes_host, uint64_t kmax, uint32_t mode, Sched sched,
                             Rec *__restrict__ recs, uint64_t *__restrict__ nchunks,
-                            unsigned long long *__restrict__ first64, int *__restrict__ err) {
+                            unsigned long long *__restrict__ first64, int *__restrict__ err,
+                            unsigned long long *__restrict__ terms) {
     const uint32_t ntests = (mode == 3) ? 2 : 1;
     const uint64_t n = n_primes_dev ? *n_primes_dev : n_primes_host;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kmax;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t i = k / ntests;
-        if (i >= n) { nchunks[k] = 0; recs[k].T = 0; recs[k].p = 0; continue; }
+        if (i >= n) { nchunks[k] = 0; recs[k].T = 0; recs[k].p = 0; continue; }   // (warp-uniform tail)
         const uint32_t test = (mode == 3) ? (uint32_t)(k % ntests) : (mode == 1 ? 0u : 1u);
         const uint64_t p = primes[i];
         const int cid = schedule(sched, p, (int)test);
@@ -117,6 +118,7 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         recs[k] = r;
         nchunks[k] = nc;
         if (p >= WIDTH32_MAX && nc > 0) atomicMin(first64, (unsigned long long)k);
+        atomicAdd(&terms[p >= WIDTH32_MAX ? 1 : 0], (unsigned long long)T);
     }
 }
 
@@ -131,52 +133,43 @@ __device__ __forceinline__ uint64_t find_rec(const uint64_t *__restrict__ start,
 }
 
 // ---------------------------------------------------------------- term runs
-// n terms s = s0, s0+1, ...: returns the pair for prod (z + s^e) in Montgomery form.
+// State of one run of consecutive terms s, s+1, ... of one sum: u = s^E and its
+// forward differences (Montgomery form), and the pair (a0, a1) of prod (z + u).
 template <class M, int E>
-__device__ __forceinline__ void run_terms(const M &mo, uint64_t s0, uint32_t n,
-                                          typename M::W &c0, typename M::W &c1) {
+struct Run {
     using W = typename M::W;
-    const W sm = mo.to(s0);
-    W u, d1, d2, d3;
-    if (E == 3) {
-        const W s2 = mo.mul(sm, sm);
-        u = mo.mul(s2, sm);
-        const W s2x3 = mo.add(mo.add(s2, s2), s2);
-        const W smx3 = mo.add(mo.add(sm, sm), sm);
-        d1 = mo.add(mo.add(s2x3, smx3), mo.r1);                  // 3s^2 + 3s + 1
-        const W smx6 = mo.add(smx3, smx3);
-        const W r1x3 = mo.add(mo.add(mo.r1, mo.r1), mo.r1);
-        const W r1x6 = mo.add(r1x3, r1x3);
-        d2 = mo.add(smx6, r1x6);                                  // 6s + 6
-        d3 = r1x6;                                                // 6
-    } else {
-        u = mo.mul(sm, sm);
-        d1 = mo.add(mo.add(sm, sm), mo.r1);                       // 2s + 1
-        d2 = mo.add(mo.r1, mo.r1);                                // 2
-        d3 = 0;
-    }
-    W a0 = mo.r1, a1 = 0;
-    uint32_t i = 0;
-    #pragma unroll 1
-    for (; i + 4 <= n; i += 4) {
-        #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            a1 = mo.muladd(a1, u, a0);
-            a0 = mo.mul(a0, u);
-            u = mo.add(u, d1);
-            d1 = mo.add(d1, d2);
-            if (E == 3) d2 = mo.add(d2, d3);
+    W u, d1, d2, d3, a0, a1;
+    __device__ __forceinline__ void setup(const M &mo, uint64_t s0) {   // s0 < p
+        const W sm = mo.mul((W)s0, mo.r2);
+        if (E == 3) {
+            const W s2 = mo.mul(sm, sm);
+            u = mo.mul(s2, sm);
+            const W s2x3 = mo.add(mo.add(s2, s2), s2);
+            const W smx3 = mo.add(mo.add(sm, sm), sm);
+            d1 = mo.add(mo.add(s2x3, smx3), mo.r1);                  // 3s^2 + 3s + 1
+            const W smx6 = mo.add(smx3, smx3);
+            const W r1x3 = mo.add(mo.add(mo.r1, mo.r1), mo.r1);
+            const W r1x6 = mo.add(r1x3, r1x3);
+            d2 = mo.add(smx6, r1x6);                                  // 6s + 6
+            d3 = r1x6;                                                // 6
+        } else {
+            u = mo.mul(sm, sm);
+            d1 = mo.add(mo.add(sm, sm), mo.r1);                       // 2s + 1
+            d2 = mo.add(mo.r1, mo.r1);                                // 2
+            d3 = 0;
         }
+        a0 = mo.r1;
+        a1 = 0;
     }
-    for (; i < n; i++) {
+    // one term of eqnComputeS: a1 <- a1 u + a0; a0 <- a0 u; then s <- s + 1
+    __device__ __forceinline__ void step(const M &mo) {
         a1 = mo.muladd(a1, u, a0);
         a0 = mo.mul(a0, u);
         u = mo.add(u, d1);
         d1 = mo.add(d1, d2);
         if (E == 3) d2 = mo.add(d2, d3);
     }
-    c0 = a0; c1 = a1;
-}
+};
 
 template <class M>
 __device__ __forceinline__ void combine(const M &mo, typename M::W &C0, typename M::W &C1,
@@ -188,6 +181,49 @@ __device__ __forceinline__ void combine(const M &mo, typename M::W &C0, typename
 
 constexpr int RES_THREADS = 256;
 constexpr int RES_WARPS = RES_THREADS / 32;
+
+// One lane's terms [t0, t1) of the record's flattened term space.  All lanes of
+// the warp advance by the same count k = min over lanes of the terms left in
+// their current run (__reduce_min_sync), so the hot loop never diverges; only
+// the switch to the next sum (fold a_j, merge, re-seed u and its differences)
+// runs on the lanes that reached a sum boundary.
+template <class M, int E>
+__device__ __forceinline__ void lane_work(const M &mo, const Cong &cg, uint64_t p, const uint64_t *first,
+                                          const uint64_t *cum, uint64_t t0, uint64_t t1,
+                                          typename M::W &C0, typename M::W &C1) {
+    using W = typename M::W;
+    Run<M, E> R;
+    uint32_t j = 0, nrun = 0;
+    if (t0 < t1) {
+        while (cum[j + 1] <= t0) j++;
+        nrun = (uint32_t)((t1 < cum[j + 1] ? t1 : cum[j + 1]) - t0);
+        R.setup(mo, first[j] + (t0 - cum[j]));
+    }
+    for (;;) {
+        const uint32_t k = __reduce_min_sync(0xffffffffu, nrun ? nrun : 0xffffffffu);
+        if (k == 0xffffffffu) break;
+        if (nrun) {
+            uint32_t i = 0;
+            #pragma unroll 1
+            for (; i + 4 <= k; i += 4) {
+                R.step(mo); R.step(mo); R.step(mo); R.step(mo);
+            }
+            for (; i < k; i++) R.step(mo);
+            nrun -= k;
+            t0 += k;
+            if (nrun == 0) {
+                const W c1 = mo.mul(R.a1, mo.mul((W)smod(cg.t[j].a, p), mo.r2));   // fold a_j
+                combine(mo, C0, C1, R.a0, c1);
+                if (t0 < t1) {
+                    j++;
+                    while (cum[j + 1] <= t0) j++;
+                    nrun = (uint32_t)((t1 < cum[j + 1] ? t1 : cum[j + 1]) - t0);
+                    R.setup(mo, first[j] + (t0 - cum[j]));
+                }
+            }
+        }
+    }
+}
 
 // Persistent: each warp pulls items g in [g_lo, g_hi) from *counter (reset to 0 before launch).
 template <class M>
@@ -235,19 +271,8 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         const uint64_t tend = base + nck;
         if (t1 > tend) t1 = tend;
         W C0 = mo.r1, C1 = 0;
-        uint32_t j = 0;
-        while (t0 < t1) {
-            while (s_cum[wid][j + 1] <= t0) j++;
-            const uint64_t se = s_cum[wid][j + 1];
-            const uint32_t n = (uint32_t)((t1 < se ? t1 : se) - t0);
-            const uint64_t s0 = s_first[wid][j] + (t0 - s_cum[wid][j]);
-            W c0, c1;
-            if (cg.e == 3) run_terms<M, 3>(mo, s0, n, c0, c1);
-            else run_terms<M, 2>(mo, s0, n, c0, c1);
-            c1 = mo.mul(c1, mo.to(smod(cg.t[j].a, r.p)));      // fold a_j
-            combine(mo, C0, C1, c0, c1);
-            t0 += n;
-        }
+        if (cg.e == 3) lane_work<M, 3>(mo, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+        else lane_work<M, 2>(mo, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             W o0 = __shfl_xor_sync(0xffffffffu, C0, o);
