@@ -183,16 +183,29 @@ int wv_schedule(uint64_t p, uint32_t test /* WV_MODE_W or WV_MODE_V */);
  *   residue_launches, records ((prime,test) pairs), chunks (warp work items). */
 typedef struct {
     uint64_t terms;
-    uint64_t terms32;          /* of which in the 32-bit (p < 2^30) kernel */
+    uint64_t terms32;          /* of which class 0: p < 2^30 (Mont32 combine) */
+    uint64_t terms_fp;         /* of which class 1: 2^30 <= p < 2^44 (FP64 engine) */
     uint64_t residue_launches;
     uint64_t records;
     uint64_t chunks;
     double   residue_ms;
-    double   residue32_ms;
+    double   residue32_ms;     /* class-0 kernel time */
+    double   residue_fp_ms;    /* class-1 kernel time */
 } wv_stats;
 int wv_stats_enable(int on);
 int wv_stats_get(wv_stats *out);
 int wv_stats_reset(void);
+
+/* Residue-kernel variants (benchmarking / tests; process-global, not
+ * thread-safe).  Primes fall in three classes: 0: p < 2^30 (32-bit
+ * Montgomery), 1: 2^30 <= p < 2^44 (FP64 engine by default), 2: p >= 2^44
+ * (64-bit Montgomery).  A variant fixes the engine (IMAD or FP64) and the
+ * number of interleaved term streams per lane.  wv_kernel_variant_info
+ * returns the name and class of variant id (WV_EINVAL past the end);
+ * wv_set_kernel_variant selects it for its class (-1 restores the default).
+ * Results are identical for every variant. */
+int wv_kernel_variant_info(int id, char *name, size_t name_cap, int *cls);
+int wv_set_kernel_variant(int cls, int id);
 
 /* Counters: kernels launched by this library since load (process-wide). */
 uint64_t wv_launch_count(void);

@@ -42,9 +42,9 @@ class _Cong(ctypes.Structure):
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("terms", ctypes.c_uint64), ("terms32", ctypes.c_uint64), ("residue_launches", ctypes.c_uint64),
-                ("records", ctypes.c_uint64), ("chunks", ctypes.c_uint64), ("residue_ms", ctypes.c_double),
-                ("residue32_ms", ctypes.c_double)]
+    _fields_ = [("terms", ctypes.c_uint64), ("terms32", ctypes.c_uint64), ("terms_fp", ctypes.c_uint64),
+                ("residue_launches", ctypes.c_uint64), ("records", ctypes.c_uint64), ("chunks", ctypes.c_uint64),
+                ("residue_ms", ctypes.c_double), ("residue32_ms", ctypes.c_double), ("residue_fp_ms", ctypes.c_double)]
 
 
 # (name, restype, argtypes) for every symbol include/wv.h declares
@@ -68,6 +68,8 @@ SIGNATURES = {
     "wv_stats_enable": (_i, [_i]),
     "wv_stats_get": (_i, [_P(Stats)]),
     "wv_stats_reset": (_i, []),
+    "wv_kernel_variant_info": (_i, [_i, ctypes.c_char_p, _sz, _P(_i)]),
+    "wv_set_kernel_variant": (_i, [_i, _i]),
     "wv_launch_count": (_u64, []),
     "wv_version": (ctypes.c_char_p, []),
     "wv_last_error": (ctypes.c_char_p, []),
@@ -260,6 +262,22 @@ def stats():
     s = Stats()
     _check(lib().wv_stats_get(ctypes.byref(s)))
     return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+
+def kernel_variants():
+    """[(id, name, class)] of the residue-kernel variants."""
+    out, i = [], 0
+    while True:
+        buf = ctypes.create_string_buffer(64)
+        c = ctypes.c_int()
+        if lib().wv_kernel_variant_info(i, buf, 64, ctypes.byref(c)) != WV_OK:
+            return out
+        out.append((i, buf.value.decode(), c.value))
+        i += 1
+
+
+def set_kernel_variant(cls, vid=-1):
+    _check(lib().wv_set_kernel_variant(cls, vid))
 
 
 def launch_count():

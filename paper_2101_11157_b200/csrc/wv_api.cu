@@ -9,6 +9,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -46,7 +47,7 @@ static Sched g_sched = {4096, C_BB1, C_BB30, C_EE3, C_EE33, -1, -1};
 static std::atomic<int> g_stats_on{0};
 static std::mutex g_stats_mu;
 static wv_stats g_stats;
-struct EvPair { cudaEvent_t a, b; bool is32; };
+struct EvPair { cudaEvent_t a, b; int cls; };
 
 static int set_err(int code, const char *fmt, ...) {
     va_list ap;
@@ -75,11 +76,45 @@ static int set_err(int code, const char *fmt, ...) {
         CK(cudaGetLastError());                                     \
     } while (0)
 
+// ------------------------------------------------------------------ residue kernel variants
+// (prime class, engine, streams per lane for e = 2 / e = 3 sums); selected per class by the
+// env vars WV_VARIANT0/1/2 (index into this table) for benchmarking; defaults below.
+typedef void (*ResKern)(const Rec *, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, ulonglong2 *,
+                        unsigned long long *, uint32_t);
+struct Variant { const char *name; int cls; ResKern fn; };
+static const Variant kVariants[] = {
+    {"c0 int s1/1", 0, residue_kernel<Mont32, 0, 0, 1, 1>},
+    {"c0 int s2/2", 0, residue_kernel<Mont32, 0, 0, 2, 2>},
+    {"c0 int s3/2", 0, residue_kernel<Mont32, 0, 0, 3, 2>},
+    {"c0 int s3/3", 0, residue_kernel<Mont32, 0, 0, 3, 3>},
+    {"c0 fp s1/1", 0, residue_kernel<Mont32, 0, 1, 1, 1>},
+    {"c1 fp s1/1", 1, residue_kernel<Mont64, 1, 1, 1, 1>},
+    {"c1 fp s2/2", 1, residue_kernel<Mont64, 1, 1, 2, 2>},
+    {"c1 int s1/1", 1, residue_kernel<Mont64, 2, 0, 1, 1>},
+    {"c2 int s1/1", 2, residue_kernel<Mont64, 2, 0, 1, 1>},
+    {"c2 int s2/2", 2, residue_kernel<Mont64, 2, 0, 2, 2>},
+};
+static const int NVAR = sizeof kVariants / sizeof kVariants[0];
+static const int kDefaultVariant[3] = {1, 6, 8};   // measured best (scripts/variant_sweep.py)
+static int g_variant[3] = {1, 6, 8};               // per class
+static void read_variant_env() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const char *names[3] = {"WV_VARIANT0", "WV_VARIANT1", "WV_VARIANT2"};
+    for (int c = 0; c < 3; c++) {
+        const char *e = getenv(names[c]);
+        if (!e) continue;
+        int v = atoi(e);
+        if (v >= 0 && v < NVAR && kVariants[v].cls == c) g_variant[c] = v;
+    }
+}
+
 // ------------------------------------------------------------------ device context
 struct DevCtx {
     bool ready = false;
     int sms = 0;
-    int occ32 = 0, occ64 = 0;
+    int occ[16] = {};            // residue-kernel blocks per SM per kernel variant
     uint32_t *d_base0 = nullptr;   // odd primes < 65536
     uint32_t nbase0 = 0;
     cudaStream_t stream = nullptr; // internal stream for the host-buffer API
@@ -100,10 +135,10 @@ static int ctx_get(DevCtx **out) {
             return set_err(WV_ECUDA, "libwv.so is built for sm_100a; device %d is sm_%d%d", dev, prop.major, prop.minor);
         c.sms = prop.multiProcessorCount;
         CK(cudaMemcpyToSymbol(c_cong, h_cong, sizeof h_cong));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ32, residue_kernel<Mont32>, RES_THREADS, 0));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ64, residue_kernel<Mont64>, RES_THREADS, 0));
-        if (c.occ32 < 1) c.occ32 = 1;
-        if (c.occ64 < 1) c.occ64 = 1;
+        for (int v = 0; v < NVAR; v++) {
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[v], kVariants[v].fn, RES_THREADS, 0));
+            if (c.occ[v] < 1) c.occ[v] = 1;
+        }
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         cudaMemPool_t pool;
         CK(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -166,8 +201,9 @@ static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static const uint64_t PART_BUDGET = 1ull << 24;   // partial pairs per batch (256 MiB)
 
-enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2, M_CNT32 = 3, M_CNT64 = 4, M_NHITS = 5, M_CHECKSUM = 6,
-       M_NBASE1 = 7, M_SPLIT = 8 /* 2 slots */, M_TERMS = 10 /* 2 slots: 32-bit, 64-bit */, M_SLOTS = 16 };
+enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2 /* 2 slots: first k with p >= 2^30, >= 2^44 */,
+       M_CNT = 4 /* 3 slots: work counters per class */, M_NHITS = 7, M_CHECKSUM = 8, M_NBASE1 = 9,
+       M_SPLIT = 10 /* 4 slots */, M_TERMS = 14 /* 3 slots: terms per class */, M_SLOTS = 24 };
 
 struct Layout {
     // problem
@@ -329,11 +365,11 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
     LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, (split g32, k64)
-    uint64_t hs[2], ht[2];
-    CK(cudaMemcpyAsync(ht, misc + M_TERMS, 16, cudaMemcpyDeviceToHost, st));
+    uint64_t hs[4], ht[3];
+    CK(cudaMemcpyAsync(ht, misc + M_TERMS, 24, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const uint64_t n = n_dev ? h[0] : n_host;
     if (n_primes_out) *n_primes_out = n;
@@ -343,12 +379,16 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     std::vector<EvPair> evs;
     if (stats) {
         std::lock_guard<std::mutex> lk(g_stats_mu);
-        g_stats.terms += ht[0] + ht[1];
+        g_stats.terms += ht[0] + ht[1] + ht[2];
         g_stats.terms32 += ht[0];
+        g_stats.terms_fp += ht[1];
         g_stats.records += K;
         g_stats.chunks += G;
     }
-    uint64_t g32 = sorted ? hs[0] : G, k64 = sorted ? hs[1] : K;   // unsorted: both kernels see everything
+    // class boundaries (sorted input): items [0,gb[1]) class 0, [gb[1],gb[2]) class 1, [gb[2],G) class 2
+    const uint64_t gb[4] = {0, sorted ? hs[0] : 0, sorted ? hs[2] : 0, G};
+    const uint64_t kbd[4] = {0, sorted ? hs[1] : 0, sorted ? hs[3] : 0, K};
+    read_variant_env();
     // batches of <= PART_BUDGET partial pairs, cut at record boundaries
     std::vector<uint64_t> hk, hg;
     if (G <= PART_BUDGET) {
@@ -368,25 +408,24 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         const uint64_t klo = hk[b], khi = hk[b + 1], glo = hg[b], ghi = hg[b + 1];
         if (khi <= klo) continue;
         // 32-bit records: items [glo, min(ghi, g32)); 64-bit: [max(glo, g32), ghi)
-        // (unsorted input: both kernels scan the whole batch and skip the other width)
-        const uint64_t a32 = glo, b32 = sorted ? (ghi < g32 ? ghi : g32) : ghi;
-        const uint64_t a64 = sorted ? (glo > g32 ? glo : g32) : glo, b64 = ghi;
-        if (b32 > a32) {
-            CK(cudaMemsetAsync(misc + M_CNT32, 0, 8, st));
-            const uint64_t khi32 = sorted ? (khi < k64 ? khi : k64) : khi;
-            EvPair ev{nullptr, nullptr, true};
+        // per class: items [max(glo, gb[c]), min(ghi, gb[c+1])) of records [max(klo,kbd[c]), min(khi,kbd[c+1]));
+        // unsorted input: every class kernel scans the whole batch and skips the other classes' records
+        for (int cls = 0; cls < 3; cls++) {
+            uint64_t a_ = glo, b_ = ghi, ka = klo, kz = khi;
+            if (sorted) {
+                a_ = glo > gb[cls] ? glo : gb[cls];
+                b_ = ghi < gb[cls + 1] ? ghi : gb[cls + 1];
+                ka = klo > kbd[cls] ? klo : kbd[cls];
+                kz = khi < kbd[cls + 1] ? khi : kbd[cls + 1];
+            }
+            if (b_ <= a_ || kz <= ka) continue;
+            CK(cudaMemsetAsync(misc + M_CNT + cls, 0, 8, st));
+            EvPair ev{nullptr, nullptr, cls};
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
-            LAUNCH(residue_kernel<Mont32>, c->sms * c->occ32, RES_THREADS, st, recs, start, klo,
-                   khi32 > klo ? khi32 : klo + 1, a32, b32, glo, part, (unsigned long long *)(misc + M_CNT32));
-            if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
-        }
-        if (b64 > a64) {
-            CK(cudaMemsetAsync(misc + M_CNT64, 0, 8, st));
-            const uint64_t klo64 = sorted ? (klo > k64 ? klo : k64) : klo;
-            EvPair ev{nullptr, nullptr, false};
-            if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
-            LAUNCH(residue_kernel<Mont64>, c->sms * c->occ64, RES_THREADS, st, recs, start, klo64, khi, a64, b64,
-                   glo, part, (unsigned long long *)(misc + M_CNT64));
+            unsigned long long *cnt = (unsigned long long *)(misc + M_CNT + cls);
+            const int var = g_variant[cls];
+            const unsigned grid = c->sms * c->occ[var];
+            LAUNCH(kVariants[var].fn, grid, RES_THREADS, st, recs, start, ka, kz, a_, b_, glo, part, cnt, 1u << cls);
             if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         const uint64_t nrec = khi - klo;
@@ -396,18 +435,20 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     }
     if (stats && !evs.empty()) {
         CK(cudaStreamSynchronize(st));
-        double ms = 0, ms32 = 0;
+        double ms = 0, ms32 = 0, msfp = 0;
         for (auto &e : evs) {
             float t = 0;
             CK(cudaEventElapsedTime(&t, e.a, e.b));
             ms += t;
-            if (e.is32) ms32 += t;
+            if (e.cls == 0) ms32 += t;
+            if (e.cls == 1) msfp += t;
             cudaEventDestroy(e.a);
             cudaEventDestroy(e.b);
         }
         std::lock_guard<std::mutex> lk(g_stats_mu);
         g_stats.residue_ms += ms;
         g_stats.residue32_ms += ms32;
+        g_stats.residue_fp_ms += msfp;
         g_stats.residue_launches += evs.size();
     }
     return WV_OK;
@@ -430,7 +471,7 @@ static int search_device_impl(const Layout &L, uint64_t *d_primes, uint64_t *d_r
     TRY(ctx_get(&c));
     uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
     CK(cudaMemsetAsync(misc, 0, M_SLOTS * 8, st));
-    CK(cudaMemsetAsync(misc + M_FIRST64, 0xff, 8, st));
+    CK(cudaMemsetAsync(misc + M_FIRST64, 0xff, 16, st));
     const uint32_t *base;
     uint32_t nbh;
     const uint64_t *nbd;
@@ -525,7 +566,7 @@ extern "C" int wv_residues_device(const uint64_t *d_primes, size_t n, uint32_t m
     int rc = WV_OK;
     do {
         if (cudaMemsetAsync(misc, 0, M_SLOTS * 8, st) != cudaSuccess ||
-            cudaMemsetAsync(misc + M_FIRST64, 0xff, 8, st) != cudaSuccess) {
+            cudaMemsetAsync(misc + M_FIRST64, 0xff, 16, st) != cudaSuccess) {
             rc = set_err(WV_ECUDA, "memset failed");
             break;
         }
@@ -716,6 +757,22 @@ extern "C" int wv_schedule(uint64_t p, uint32_t test) {
 
 extern "C" uint64_t wv_launch_count(void) { return g_launches.load(); }
 
+extern "C" int wv_kernel_variant_info(int id, char *name, size_t name_cap, int *cls) {
+    if (id < 0 || id >= NVAR) return set_err(WV_EINVAL, "variant %d out of range", id);
+    if (name && name_cap) snprintf(name, name_cap, "%s", kVariants[id].name);
+    if (cls) *cls = kVariants[id].cls;
+    return WV_OK;
+}
+
+extern "C" int wv_set_kernel_variant(int cls, int id) {
+    if (cls < 0 || cls > 2) return set_err(WV_EINVAL, "class %d", cls);
+    read_variant_env();
+    if (id < 0) { g_variant[cls] = kDefaultVariant[cls]; return WV_OK; }
+    if (id >= NVAR || kVariants[id].cls != cls) return set_err(WV_EINVAL, "variant %d is not for class %d", id, cls);
+    g_variant[cls] = id;
+    return WV_OK;
+}
+
 extern "C" int wv_stats_enable(int on) {
     g_stats_on.store(on ? 1 : 0);
     return WV_OK;
@@ -733,7 +790,7 @@ extern "C" int wv_stats_reset(void) {
 }
 
 extern "C" const char *wv_version(void) {
-    return "libwv 0.1 (sm_100a; Mont32 p<2^30, Mont64 p<2^62; sieve+plan+residue+finalize)";
+    return "libwv 0.2 (sm_100a; Mont32 p<2^30 | FP64 EFT p<2^44 | Mont64 p<2^62; sieve+plan+residue+finalize)";
 }
 
 extern "C" const char *wv_last_error(void) { return g_err; }

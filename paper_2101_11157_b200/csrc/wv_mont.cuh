@@ -91,6 +91,49 @@ struct Mont64 {
     }
 };
 
+// Exact modular arithmetic on the FP64 pipe (p < 2^44), a second engine beside
+// the IMAD path.  Values are doubles holding integers; a product uses the
+// error-free transform  a b = h + l  (h = fl(a b), l = fma(a, b, -h) exact),
+// q = rint(h / p) via fma(h, 1/p, 1.5*2^52) - 1.5*2^52, and
+//     a b - q p = fma(-q, p, h) + l        (both steps exact),
+// so the result is congruent to a b mod p with |result| <= p whenever
+// |a| <= 2p and |b| <= 2^49 (then q < 2^51, |q - h/p| <= 0.875 and
+// |l| <= 2^-53 |h| <= p/8).  Residues stay "balanced" (signed) -- no
+// conditional corrections in the hot loop.  All operations use _rn
+// intrinsics so the compiler cannot re-associate or contract them.
+struct ModD {
+    double p, pinv;
+    uint32_t rb2, rb3;      // reduction intervals (terms) for e = 2 and e = 3
+    static constexpr double MAGIC = 6755399441055744.0;   // 1.5 * 2^52
+
+    __device__ __forceinline__ void init(uint64_t p64) {
+        p = (double)p64;
+        pinv = __drcp_rn(p);
+        const int lg = 64 - __clzll(p64);                  // p < 2^lg
+        // e = 2: u grows by < p per term from <= p:      u <= (1 + j) p + j^2  <= 2^49
+        // e = 3: d1 grows by < 3p+6j, u by d1:           u <= (1 + j + 4.5 j^2) p <= 2^49
+        const int k2 = 48 - lg, k3 = (46 - lg) / 2;
+        rb2 = k2 >= 20 ? (1u << 20) : (k2 < 1 ? 1u : (1u << k2));
+        rb3 = k3 >= 20 ? (1u << 20) : (k3 < 1 ? 1u : (1u << k3));
+    }
+    __device__ __forceinline__ double rnd(double x) const {   // rint(x / p) for |x| < 2^51 p
+        return __dadd_rn(__fma_rn(x, pinv, MAGIC), -MAGIC);
+    }
+    __device__ __forceinline__ double mul(double a, double b) const {
+        const double h = __dmul_rn(a, b);
+        const double l = __fma_rn(a, b, -h);
+        const double q = rnd(h);
+        return __dadd_rn(__fma_rn(-q, p, h), l);
+    }
+    __device__ __forceinline__ double reduce(double x) const { return __fma_rn(-rnd(x), p, x); }
+    __device__ __forceinline__ uint64_t canon(double x) const {
+        double r = reduce(x);
+        if (r < 0) r = __dadd_rn(r, p);
+        if (r >= p) r = __dadd_rn(r, -p);
+        return (uint64_t)r;
+    }
+};
+
 // signed integer -> residue in [0, p)   (no division when |a| < p)
 __device__ __forceinline__ uint64_t smod(int64_t a, uint64_t p) {
     uint64_t m = a >= 0 ? (uint64_t)a : (uint64_t)(-a);

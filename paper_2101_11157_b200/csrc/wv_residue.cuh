@@ -55,6 +55,8 @@ struct Sched {              // default schedule + overrides
 constexpr uint32_t CAP_CHUNKS = 1024;   // target max chunks per record
 constexpr uint32_t LMIN = 4096;         // min terms per lane in a full chunk
 constexpr uint64_t WIDTH32_MAX = 1ull << 30;  // Mont32 (lazy, fused) needs p < 2^30
+constexpr uint64_t FP64_MAX = 1ull << 44;     // ModD (FP64 engine) needs p < 2^44
+__host__ __device__ __forceinline__ int prime_class(uint64_t p) { return p < WIDTH32_MAX ? 0 : (p < FP64_MAX ? 1 : 2); }
 
 // ids in congruences.inc order
 enum { C_VOR12 = 0, C_BB1 = 1, C_BB2, C_BB6, C_BB9, C_BB16, C_BB22, C_BB30,
@@ -118,7 +120,8 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         recs[k] = r;
         nchunks[k] = nc;
         if (p >= WIDTH32_MAX && nc > 0) atomicMin(first64, (unsigned long long)k);
-        atomicAdd(&terms[p >= WIDTH32_MAX ? 1 : 0], (unsigned long long)T);
+        if (p >= FP64_MAX && nc > 0) atomicMin(first64 + 1, (unsigned long long)k);
+        atomicAdd(&terms[prime_class(p)], (unsigned long long)T);
     }
 }
 
@@ -133,13 +136,18 @@ __device__ __forceinline__ uint64_t find_rec(const uint64_t *__restrict__ start,
 }
 
 // ---------------------------------------------------------------- term runs
-// State of one run of consecutive terms s, s+1, ... of one sum: u = s^E and its
-// forward differences (Montgomery form), and the pair (a0, a1) of prod (z + u).
+// A "run" is the state of consecutive terms s, s+1, ... of one sum: u = s^E,
+// its forward differences, and the pair (a0, a1) of prod (z + u).  Two
+// engines implement the same interface (setup / step / reduce / result):
+//   Run<M,E>  -- Montgomery products on the IMAD pipe (lazy values in [0,2p));
+//   RunD<E>   -- exact FP64 error-free-transform products (ModD, p < 2^44) on
+//                the DFMA pipe, balanced values, periodic range reduction.
 template <class M, int E>
 struct Run {
     using W = typename M::W;
+    static constexpr bool kFP = false;
     W u, d1, d2, d3, a0, a1;
-    __device__ __forceinline__ void setup(const M &mo, uint64_t s0) {   // s0 < p
+    __device__ __forceinline__ void setup(const M &mo, const ModD &, uint64_t s0) {   // s0 < p
         const W sm = mo.mul((W)s0, mo.r2);
         if (E == 3) {
             const W s2 = mo.mul(sm, sm);
@@ -162,12 +170,51 @@ struct Run {
         a1 = 0;
     }
     // one term of eqnComputeS: a1 <- a1 u + a0; a0 <- a0 u; then s <- s + 1
-    __device__ __forceinline__ void step(const M &mo) {
+    __device__ __forceinline__ void step(const M &mo, const ModD &) {
         a1 = mo.muladd(a1, u, a0);
         a0 = mo.mul(a0, u);
         u = mo.add(u, d1);
         d1 = mo.add(d1, d2);
         if (E == 3) d2 = mo.add(d2, d3);
+    }
+    __device__ __forceinline__ void reduce(const ModD &) {}
+    __device__ __forceinline__ void result(const M &, const ModD &, W &c0, W &c1) const { c0 = a0; c1 = a1; }
+};
+
+template <class M, int E>
+struct RunD {
+    using W = typename M::W;
+    static constexpr bool kFP = true;
+    double u, d1, d2, a0, a1;
+    __device__ __forceinline__ void setup(const M &, const ModD &md, uint64_t s0) {   // s0 < p/2
+        const double s = (double)s0;
+        if (E == 3) {
+            const double s2 = md.mul(s, s);                                    // |s2| <= p
+            u = md.mul(s2, s);
+            d1 = md.reduce(__fma_rn(3.0, __dadd_rn(s2, s), 1.0));              // 3s^2 + 3s + 1 (< 2^47: exact)
+            d2 = __fma_rn(6.0, s, 6.0);                                        // 6s + 6, exact
+        } else {
+            u = md.mul(s, s);
+            d1 = __fma_rn(2.0, s, 1.0);                                        // 2s + 1 < p, exact
+            d2 = 2.0;
+        }
+        a0 = 1.0;
+        a1 = 0.0;
+    }
+    __device__ __forceinline__ void step(const M &, const ModD &md) {
+        a1 = __dadd_rn(md.mul(a1, u), a0);       // |a1| <= 2p
+        a0 = md.mul(a0, u);                      // |a0| <= p
+        u = __dadd_rn(u, d1);
+        d1 = __dadd_rn(d1, d2);
+        if (E == 3) d2 = __dadd_rn(d2, 6.0);
+    }
+    __device__ __forceinline__ void reduce(const ModD &md) {
+        u = md.reduce(u);
+        if (E == 3) d1 = md.reduce(d1);
+    }
+    __device__ __forceinline__ void result(const M &mo, const ModD &md, W &c0, W &c1) const {
+        c0 = mo.mul((W)md.canon(a0), mo.r2);     // into the combine domain (Montgomery form)
+        c1 = mo.mul((W)md.canon(a1), mo.r2);
     }
 };
 
@@ -182,55 +229,106 @@ __device__ __forceinline__ void combine(const M &mo, typename M::W &C0, typename
 constexpr int RES_THREADS = 256;
 constexpr int RES_WARPS = RES_THREADS / 32;
 
-// One lane's terms [t0, t1) of the record's flattened term space.  All lanes of
-// the warp advance by the same count k = min over lanes of the terms left in
-// their current run (__reduce_min_sync), so the hot loop never diverges; only
-// the switch to the next sum (fold a_j, merge, re-seed u and its differences)
-// runs on the lanes that reached a sum boundary.
-template <class M, int E>
-__device__ __forceinline__ void lane_work(const M &mo, const Cong &cg, uint64_t p, const uint64_t *first,
-                                          const uint64_t *cum, uint64_t t0, uint64_t t1,
+// One lane's terms [t0, t1) of the record's flattened term space, split into S
+// contiguous "streams" (independent runs interleaved in one instruction stream
+// for ILP: a single Montgomery stream is dependency-latency bound on sm_100a).
+// All lanes and streams advance by the same count k = the minimum, over the
+// warp, of the terms left in any active run (__reduce_min_sync), so the hot
+// loop never diverges; only the switch to the next sum (fold a_j, merge,
+// re-seed u and its differences) runs where a run ended.  Finished streams keep
+// stepping on dead state (ignored).  The FP64 engine range-reduces its u (and
+// d1) every rb terms, counted warp-uniformly.
+template <class M, class R, int E, int S>
+__device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Cong &cg, uint64_t p,
+                                          const uint64_t *first, const uint64_t *cum, uint64_t t0, uint64_t t1,
                                           typename M::W &C0, typename M::W &C1) {
     using W = typename M::W;
-    Run<M, E> R;
-    uint32_t j = 0, nrun = 0;
-    if (t0 < t1) {
-        while (cum[j + 1] <= t0) j++;
-        nrun = (uint32_t)((t1 < cum[j + 1] ? t1 : cum[j + 1]) - t0);
-        R.setup(mo, first[j] + (t0 - cum[j]));
+    R run[S];
+    uint32_t j[S], nrun[S];
+    uint64_t t[S], te[S];
+    const uint32_t rb = R::kFP ? (E == 3 ? md.rb3 : md.rb2) : 0xffffffffu;
+    uint32_t since = 0;
+    const uint64_t len = t1 > t0 ? t1 - t0 : 0;
+    const uint64_t q = (len + S - 1) / S;
+    #pragma unroll
+    for (int i = 0; i < S; i++) {
+        t[i] = t0 + i * q;
+        te[i] = t[i] + q < t1 ? t[i] + q : t1;
+        j[i] = 0;
+        nrun[i] = 0;
+        if (t[i] < te[i]) {
+            while (cum[j[i] + 1] <= t[i]) j[i]++;
+            nrun[i] = (uint32_t)((te[i] < cum[j[i] + 1] ? te[i] : cum[j[i] + 1]) - t[i]);
+            run[i].setup(mo, md, first[j[i]] + (t[i] - cum[j[i]]));
+        } else {
+            run[i].setup(mo, md, 1);          // dead stream: defined state
+        }
     }
     for (;;) {
-        const uint32_t k = __reduce_min_sync(0xffffffffu, nrun ? nrun : 0xffffffffu);
+        uint32_t mn = 0xffffffffu;
+        #pragma unroll
+        for (int i = 0; i < S; i++)
+            if (nrun[i] && nrun[i] < mn) mn = nrun[i];
+        const uint32_t k = __reduce_min_sync(0xffffffffu, mn);
         if (k == 0xffffffffu) break;
-        if (nrun) {
+        uint32_t left = k;
+        while (left) {
+            const uint32_t kk = left < rb - since ? left : rb - since;
             uint32_t i = 0;
             #pragma unroll 1
-            for (; i + 4 <= k; i += 4) {
-                R.step(mo); R.step(mo); R.step(mo); R.step(mo);
+            for (; i + 4 <= kk; i += 4) {
+                #pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    #pragma unroll
+                    for (int s_ = 0; s_ < S; s_++) run[s_].step(mo, md);
+                }
             }
-            for (; i < k; i++) R.step(mo);
-            nrun -= k;
-            t0 += k;
-            if (nrun == 0) {
-                const W c1 = mo.mul(R.a1, mo.mul((W)smod(cg.t[j].a, p), mo.r2));   // fold a_j
-                combine(mo, C0, C1, R.a0, c1);
-                if (t0 < t1) {
-                    j++;
-                    while (cum[j + 1] <= t0) j++;
-                    nrun = (uint32_t)((t1 < cum[j + 1] ? t1 : cum[j + 1]) - t0);
-                    R.setup(mo, first[j] + (t0 - cum[j]));
+            for (; i < kk; i++) {
+                #pragma unroll
+                for (int s_ = 0; s_ < S; s_++) run[s_].step(mo, md);
+            }
+            left -= kk;
+            if (R::kFP) {
+                since += kk;
+                if (since == rb) {
+                    #pragma unroll
+                    for (int s_ = 0; s_ < S; s_++) run[s_].reduce(md);
+                    since = 0;
+                }
+            }
+        }
+        #pragma unroll
+        for (int i = 0; i < S; i++) {
+            if (!nrun[i]) continue;
+            nrun[i] -= k;
+            t[i] += k;
+            if (nrun[i] == 0) {
+                W c0, c1;
+                run[i].result(mo, md, c0, c1);
+                c1 = mo.mul(c1, mo.mul((W)smod(cg.t[j[i]].a, p), mo.r2));   // fold a_j
+                combine(mo, C0, C1, c0, c1);
+                if (t[i] < te[i]) {
+                    j[i]++;
+                    while (cum[j[i] + 1] <= t[i]) j[i]++;
+                    nrun[i] = (uint32_t)((te[i] < cum[j[i] + 1] ? te[i] : cum[j[i] + 1]) - t[i]);
+                    run[i].setup(mo, md, first[j[i]] + (t[i] - cum[j[i]]));
                 }
             }
         }
     }
 }
 
+// Prime classes: 0: p < 2^30 (Mont32 combine; IMAD or FP64 runs)
+//                1: 2^30 <= p < 2^44 (Mont64 combine; FP64 or IMAD runs)
+//                2: p >= 2^44 (Mont64, IMAD runs only)
+
+// ENGINE: 0 = IMAD runs, 1 = FP64 runs;  S = streams per lane (E = 2 / E = 3 sums)
 // Persistent: each warp pulls items g in [g_lo, g_hi) from *counter (reset to 0 before launch).
-template <class M>
+template <class M, int CLASS, int ENGINE, int S2, int S3>
 __global__ void __launch_bounds__(RES_THREADS)
 residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
                uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
-               unsigned long long *__restrict__ counter) {
+               unsigned long long *__restrict__ counter, uint32_t class_mask) {
     using W = typename M::W;
     __shared__ uint64_t s_first[RES_WARPS][34];
     __shared__ uint64_t s_cum[RES_WARPS][35];
@@ -243,7 +341,7 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         if (g >= g_hi) break;
         const uint64_t k = find_rec(start, klo, khi, g);
         const Rec r = recs[k];
-        if ((r.p >= WIDTH32_MAX) != (sizeof(W) == 8)) continue;   // the other width's kernel does it
+        if (!((class_mask >> prime_class(r.p)) & 1)) continue;   // another class's launch does it
         const uint64_t c = g - start[k];
         const Cong &cg = c_cong[r.cid];
         const uint32_t m = cg.m;
@@ -271,8 +369,15 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         const uint64_t tend = base + nck;
         if (t1 > tend) t1 = tend;
         W C0 = mo.r1, C1 = 0;
-        if (cg.e == 3) lane_work<M, 3>(mo, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
-        else lane_work<M, 2>(mo, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+        ModD md;
+        if (ENGINE == 1) {
+            md.init(r.p);
+            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            else lane_work<M, RunD<M, 2>, 2, S2>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+        } else {
+            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            else lane_work<M, Run<M, 2>, 2, S2>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+        }
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             W o0 = __shfl_xor_sync(0xffffffffu, C0, o);
@@ -389,12 +494,14 @@ __global__ void pack_residues_kernel(const uint64_t *__restrict__ primes, uint64
 }
 
 // first item of the first 64-bit record, and the batch boundaries
-__global__ void split_kernel(const uint64_t *__restrict__ start, uint64_t K, const unsigned long long *first64,
+__global__ void split_kernel(const uint64_t *__restrict__ start, uint64_t K, const unsigned long long *first,
                              uint64_t *__restrict__ out) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
-        unsigned long long k = *first64;
-        out[0] = (k >= K) ? start[K] : start[k];   // start has K+1 entries (start[K] = total)
-        out[1] = (k >= K) ? K : k;
+        for (int c = 0; c < 2; c++) {              // class boundaries 2^30 and 2^44
+            unsigned long long k = first[c];
+            out[2 * c] = (k >= K) ? start[K] : start[k];   // start has K+1 entries (start[K] = total)
+            out[2 * c + 1] = (k >= K) ? K : k;
+        }
     }
 }
 

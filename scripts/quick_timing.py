@@ -19,4 +19,7 @@ for name in names:
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
-    print(f"{name}: {ds.n_primes} primes, {ds.n_hits} hits, {ms:.3f} ms/run, {ds.n_primes / ms * 1e3:.1f} primes/s", flush=True)
+    wv.stats_reset(); wv.stats_enable(True); ds.run(); wv.stats_enable(False); st = wv.stats()
+    tps = st["terms"] / (st["residue_ms"] / 1e3) if st["residue_ms"] else 0
+    print(f"{name}: {ds.n_primes} primes, {ds.n_hits} hits, {ms:.3f} ms/run, {ds.n_primes / ms * 1e3:.1f} primes/s, "
+          f"residue {st['residue_ms']:.2f} ms, {tps:.3e} terms/s, chk {ds.checksum_int():016x}", flush=True)

@@ -237,3 +237,60 @@ def test_ragged_tail_64bit_window(wv):
     w = SUBWINDOWS["c4_head"]
     hits, res = wv.search(w.lo, w.hi, w.mode)
     assert res["p"].tolist() == oracle.primes(w.lo, w.hi)
+
+
+def test_kernel_variants_bit_identical(wv):
+    """Every residue-kernel variant (engine x streams per lane) gives the same residues:
+    a window spanning the 2^30 class boundary plus Table 2/3 primes (class 1)."""
+    lo, hi = (1 << 30) - 20000, (1 << 30) + 20000
+    ref_h, ref_r = wv.search(lo, hi, 3)
+    tab = [1025793739, 1348936931, 10158743171, 56604583391]
+    ref_w, ref_v = wv.residues_of(tab, 3)
+    try:
+        for vid, name, cls in wv.kernel_variants():
+            if cls == 2:
+                continue
+            wv.set_kernel_variant(cls, vid)
+            h, r = wv.search(lo, hi, 3)
+            assert r.tobytes() == ref_r.tobytes(), name
+            rw, rv = wv.residues_of(tab, 3)
+            assert rw.tolist() == ref_w.tolist() and rv.tolist() == ref_v.tolist(), name
+            wv.set_kernel_variant(cls, -1)
+    finally:
+        for c in range(3):
+            wv.set_kernel_variant(c, -1)
+
+
+def test_class2_64bit_montgomery_cross_congruence(wv):
+    """p >= 2^44 runs the 64-bit Montgomery engine: two different congruences agree
+    (BB1 vs BB30 for W, EE3 vs EE33 for V) on a prime just above 2^44 (property check)."""
+    p = 17592186044423          # smallest prime > 2^44
+    names = {c["name"]: c["id"] for c in wv.congruences()}
+    out = {}
+    try:
+        for w, v in [("BB1", "EE3"), ("BB30", "EE33")]:
+            wv.set_schedule_override(names[w], names[v])
+            rw, rv = wv.residues_of([p], 3)
+            out[w] = (int(rw[0]), int(rv[0]))
+    finally:
+        wv.set_schedule_override(-1, -1)
+    assert out["BB1"] == out["BB30"]
+    assert 0 <= out["BB1"][0] < p and 0 <= out["BB1"][1] < p
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_c4_c5_sampled_primes(wv, name):
+    """configs[3], configs[4]: the oracle's deterministic 8-prime samples of the full windows
+    (p ~ 5.9e10 and 3.9e10: the FP64-engine class), bit-exact; also through the sieve path
+    on the first sample's neighbourhood."""
+    gp, gw, gv, meta = _golden(name)
+    w = CONFIGS[name]
+    rw, rv = wv.residues_of(gp.tolist(), w.mode)
+    if w.mode & 1:
+        _assert_equal(gp, rw, gw, f"{name} W")
+    if w.mode & 2:
+        _assert_equal(gp, rv, gv, f"{name} V")
+    p0 = int(gp[0])
+    hits, res = wv.search(p0, p0 + 1, w.mode)
+    assert res["p"].tolist() == [p0]
+    assert (int(res["res_w"][0]) if w.mode & 1 else NONE) == int(gw[0])
