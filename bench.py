@@ -38,12 +38,14 @@ sys.path.insert(0, ROOT)
 METRIC = "primes tested/sec (W+V)"
 UNIT = "primes/s"
 
-# Montgomery multiplications per term: c1 <- c1 u + c0, c0 <- c0 u
+# Modular multiplications per term: c1 <- c1 u + c0, c0 <- c0 u
 MULMODS_PER_TERM = 2
-# 32-bit multiplies (IMAD-class) per Montgomery product: Mont32 = 3 (a*b wide, m = lo*p', hi(m*p));
-# Mont64 = 11 (4 partial products for a*b, 3 for lo64(lo*p'), 4 for hi(m*p)).  DESIGN.md "Roofline".
-IMUL_PER_MULMOD = {32: 3, 64: 11}
-IMAD_PER_CLK_PER_SM = 64      # FMA-heavy pipe: 16 lanes/clk/SMSP x 4 SMSP (B300_MICROARCH.md "Pipe rates")
+# Roofline per prime class: (pipe, lanes/clk/SM, pipe slots per modular product)
+#   class 0 (p < 2^30, Mont32): fmaheavy pipe, 64 IMAD/clk/SM (guide: rt_SMSP = 2);
+#            IMAD.WIDE 2 + IMAD 1 + IMAD.HI 2 = 5 slots per product (WIDE/HI measured at half rate)
+#   class 1 (2^30 <= p < 2^44, FP64 EFT): fp64 pipe, 64 DFMA/clk/SM; 6 DP ops per product
+#   class 2 (p >= 2^44, Mont64): fmaheavy, ~22 slots per product (11 wide/high 32-bit partial products)
+ROOF = {0: ("fmaheavy", 64, 5), 1: ("fp64", 64, 6), 2: ("fmaheavy", 64, 22)}
 
 
 def _env_int(name, default):
@@ -77,7 +79,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                          "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
 
@@ -276,28 +278,42 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel: residue_kernel (Mont32 for C1-C3 windows, Mont64 above 2^30)
+    # roofline of the dominant kernel: the residue kernel of the class with the most device time
     peaks, peak_kind = _peaks()
     steps = args.steps
-    terms = st["terms"] / steps
-    terms32 = st["terms32"] / steps
-    res_ms = st["residue_ms"] / steps
-    res32_ms = st["residue32_ms"] / steps
-    width = 32 if terms32 >= terms - terms32 else 64
-    k_terms = terms32 if width == 32 else terms - terms32
-    k_ms = res32_ms if width == 32 else res_ms - res32_ms
+    cls_terms = {0: st["terms32"] / steps, 1: st["terms_fp"] / steps,
+                 2: (st["terms"] - st["terms32"] - st["terms_fp"]) / steps}
+    cls_ms = {0: st["residue32_ms"] / steps, 1: st["residue_fp_ms"] / steps,
+              2: (st["residue_ms"] - st["residue32_ms"] - st["residue_fp_ms"]) / steps}
+    cls = max(cls_ms, key=lambda c: cls_ms[c])
+    k_terms, k_ms = cls_terms[cls], cls_ms[cls]
     mhz = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak_imul = IMAD_PER_CLK_PER_SM * sms * mhz * 1e6
-    peak_mulmod = peak_imul / IMUL_PER_MULMOD[width]
+    pipe, lanes, slots = ROOF[cls]
+    peak_mulmod = lanes * sms * mhz * 1e6 / slots
     achieved = MULMODS_PER_TERM * k_terms / (k_ms / 1e3) if k_ms > 0 else 0.0
-    roof = {"bound": "alu", "kernel": f"residue_kernel<Mont{width}>", "achieved": achieved / 1e9,
-            "peak": peak_mulmod / 1e9, "unit": "Gmulmod/s", "frac": achieved / peak_mulmod if peak_mulmod else None,
-            "traffic": None,
-            "peak_basis": f"{IMAD_PER_CLK_PER_SM} IMAD/clk/SM x {sms} SMs x {mhz:.0f} MHz ({peak_kind} sm_max_mhz) "
-                          f"/ {IMUL_PER_MULMOD[width]} IMAD per Mont{width} product",
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"r1_{args.workload}_residue_kernel_full.txt")
+    if os.path.exists(prof):
+        rd = wr = None
+        for line in open(prof):
+            f = line.split()
+            if line.strip().startswith("dram bytes read"):
+                rd = float(f[3]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(f[4], 1)
+            if line.strip().startswith("dram bytes write"):
+                wr = float(f[3]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(f[4], 1)
+        if rd is not None and wr is not None:
+            traffic = rd + wr
+    kname = {0: "residue_kernel<Mont32> (class 0, p < 2^30)", 1: "residue_kernel<Mont64, FP64 engine> (class 1)",
+             2: "residue_kernel<Mont64> (class 2, p >= 2^44)"}[cls]
+    roof = {"bound": "alu", "kernel": kname, "achieved": achieved / 1e9, "peak": peak_mulmod / 1e9,
+            "unit": "Gmulmod/s", "frac": achieved / peak_mulmod if peak_mulmod else None, "traffic": traffic,
+            "traffic_unit": "bytes/launch (DRAM read+write, ncu --set full, profiles/)",
+            "peak_basis": f"{pipe} pipe: {lanes} lanes/clk/SM x {sms} SMs x {mhz:.0f} MHz ({peak_kind} sm_max_mhz) "
+                          f"/ {slots} pipe slots per modular product",
+            "peak_guide_3imad": lanes * sms * mhz * 1e6 / 3 / 1e9 if cls == 0 else None,
             "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms_max if ms_max else None,
-            "terms_per_step": terms, "terms_per_s": k_terms / (k_ms / 1e3) if k_ms > 0 else None}
+            "terms_per_step": sum(cls_terms.values()), "kernel_terms_per_s": k_terms / (k_ms / 1e3) if k_ms else None}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -308,11 +324,12 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u32" if width == 32 else "u64", "data": "synthetic",
+            "vs_baseline": None, "dtype": {0: "u32", 1: "f64", 2: "u64"}[cls], "data": "synthetic",
             "config": {"workload": w.name, "window": [w.lo, w.hi], "mode": {1: "W", 2: "V", 3: "W+V"}[w.mode],
                        "primes": n_all, "parallelism": f"interleaved blocks x{world}",
                        "l2_flush": "256 MiB write between timed steps (outside the CUDA events)",
-                       "terms_per_step": terms, "mulmods_per_s": MULMODS_PER_TERM * terms / (ms_max / 1e3)},
+                       "terms_per_step": sum(cls_terms.values()),
+                       "mulmods_per_s": MULMODS_PER_TERM * sum(cls_terms.values()) / (ms_max / 1e3)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk}
     print(json.dumps(line), flush=True)

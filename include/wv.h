@@ -140,6 +140,14 @@ int wv_sieve_device(uint64_t lo, uint64_t hi, uint64_t *d_primes, size_t cap, si
  * the paper's counts).  Device scratch is internal. */
 int wv_prime_count(uint64_t lo, uint64_t hi, uint64_t *count);
 
+/* wv_shard_blocks: host-only (no GPU) description of the interleaved partition
+ * used by wv_search_shard: writes the integer ranges [lo_i, hi_i) of this
+ * shard's blocks (clipped to [lo, hi), empty ones skipped) into out[2*i],
+ * out[2*i+1] for i < cap, sets *n to their number and *block_used to the block
+ * size actually used (the default when block == 0).  WV_ENOSPC if cap < *n. */
+int wv_shard_blocks(uint64_t lo, uint64_t hi, uint32_t shard, uint32_t nshards, uint64_t block,
+                    uint64_t *out, size_t cap, size_t *n, uint64_t *block_used);
+
 /* ------------------------------------------------------ small utilities */
 
 /* Checksum term of one prime (reading R6 in DESIGN.md):

@@ -60,6 +60,7 @@ SIGNATURES = {
     "wv_residues_device": (_i, [_vp, _sz, _u32, _vp, _vp, _vp, _sz, _vp]),
     "wv_sieve_device": (_i, [_u64, _u64, _vp, _sz, _P(_sz), _vp, _sz, _vp]),
     "wv_prime_count": (_i, [_u64, _u64, _P(_u64)]),
+    "wv_shard_blocks": (_i, [_u64, _u64, _u32, _u32, _u64, _vp, _sz, _P(_sz), _P(_u64)]),
     "wv_checksum_term": (_u64, [_u64, _u64, _u64]),
     "wv_congruence_count": (_i, []),
     "wv_congruence_get": (_i, [_i, _P(_Cong)]),
@@ -223,6 +224,16 @@ def prime_count(lo, hi):
     c = ctypes.c_uint64()
     _check(lib().wv_prime_count(lo, hi, ctypes.byref(c)))
     return int(c.value)
+
+
+def shard_blocks(lo, hi, shard, nshards, block=0):
+    """Host-only: ([(a, b), ...] integer ranges of this shard's blocks, block size used)."""
+    L = lib()
+    n, bu = ctypes.c_size_t(), ctypes.c_uint64()
+    _check(L.wv_shard_blocks(lo, hi, shard, nshards, block, None, 0, ctypes.byref(n), ctypes.byref(bu)))
+    buf = np.zeros(2 * max(n.value, 1), dtype=np.uint64)
+    _check(L.wv_shard_blocks(lo, hi, shard, nshards, block, _ptr(buf), n.value, ctypes.byref(n), ctypes.byref(bu)))
+    return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)], int(bu.value)
 
 
 # ------------------------------------------------------------------ small utilities

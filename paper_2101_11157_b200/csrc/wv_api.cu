@@ -729,6 +729,24 @@ extern "C" int wv_search_shard(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t
                        n_primes, checksum);
 }
 
+extern "C" int wv_shard_blocks(uint64_t lo, uint64_t hi, uint32_t shard, uint32_t nshards, uint64_t block,
+                               uint64_t *out, size_t cap, size_t *n, uint64_t *block_used) {
+    Layout L;
+    TRY(make_layout(lo, hi, 1, shard, nshards, block, L));
+    const uint64_t nblocks = (hi - lo + L.block - 1) / L.block;
+    size_t k = 0;
+    for (uint64_t b = shard; b < nblocks; b += nshards) {
+        const uint64_t a_ = lo + b * L.block, z = a_ + L.block < hi ? a_ + L.block : hi;
+        if (z <= a_) continue;
+        if (out && k < cap) { out[2 * k] = a_; out[2 * k + 1] = z; }
+        k++;
+    }
+    if (n) *n = k;
+    if (block_used) *block_used = L.block;
+    if (out && k > cap) return set_err(WV_ENOSPC, "cap %zu < %zu blocks", cap, k);
+    return WV_OK;
+}
+
 // ------------------------------------------------------------------ utilities
 extern "C" uint64_t wv_checksum_term(uint64_t p, uint64_t res_w, uint64_t res_v) { return checksum_term(p, res_w, res_v); }
 
