@@ -114,18 +114,41 @@ def search(lo: int, hi: int, mode: int = MODE_BOTH, residues: bool = True):
     return search_shard(lo, hi, mode, 0, 1, 0, residues)[:2]
 
 
-def search_shard(lo: int, hi: int, mode: int, shard: int, nshards: int, block: int = 0, residues: bool = True):
-    """wv_search_shard: returns (hits, residues or None, checksum)."""
+def search_shard(lo: int, hi: int, mode: int, shard: int, nshards: int, block: int = 0, residues: bool = True,
+                 hits_out: np.ndarray | None = None, res_out: np.ndarray | None = None):
+    """wv_search_shard: returns (hits, residues or None, checksum).
+
+    hits_out / res_out: optional caller buffers (HIT_DTYPE / RES_DTYPE arrays, e.g. views of pinned
+    memory from pinned_buffers()) with room for prime_cap entries; the results are views into them."""
     L = lib()
     ws, cap = ctypes.c_size_t(), ctypes.c_size_t()
     _check(L.wv_device_workspace_bytes(lo, hi, mode, shard, nshards, block, ctypes.byref(ws), ctypes.byref(cap)))
     n = max(int(cap.value), 1)
-    hits = np.zeros(n, dtype=HIT_DTYPE)
-    res = np.zeros(n, dtype=RES_DTYPE) if residues else None
+    hits = hits_out if hits_out is not None and len(hits_out) >= n else np.zeros(n, dtype=HIT_DTYPE)
+    res = None
+    if residues:
+        res = res_out if res_out is not None and len(res_out) >= n else np.zeros(n, dtype=RES_DTYPE)
     nh, npr, chk = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_uint64()
-    _check(L.wv_search_shard(lo, hi, mode, shard, nshards, block, _ptr(hits), n, ctypes.byref(nh), _ptr(res),
-                             n if residues else 0, ctypes.byref(npr), ctypes.byref(chk)))
-    return hits[: nh.value].copy(), (res[: npr.value].copy() if residues else None), int(chk.value)
+    _check(L.wv_search_shard(lo, hi, mode, shard, nshards, block, _ptr(hits), len(hits), ctypes.byref(nh), _ptr(res),
+                             len(res) if residues else 0, ctypes.byref(npr), ctypes.byref(chk)))
+    hv = hits[: nh.value] if hits is hits_out else hits[: nh.value].copy()
+    rv = None
+    if residues:
+        rv = res[: npr.value] if res is res_out else res[: npr.value].copy()
+    return hv, rv, int(chk.value)
+
+
+def pinned_buffers(lo: int, hi: int, mode: int = MODE_BOTH, shard: int = 0, nshards: int = 1, block: int = 0):
+    """Page-locked (torch pin_memory) host buffers sized for wv_search_shard over this window."""
+    import torch
+    ws, cap = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().wv_device_workspace_bytes(lo, hi, mode, shard, nshards, block, ctypes.byref(ws), ctypes.byref(cap)))
+    n = max(int(cap.value), 1)
+    th = torch.empty(n * HIT_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+    tr = torch.empty(n * RES_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+    hits = th.numpy().view(HIT_DTYPE)
+    res = tr.numpy().view(RES_DTYPE)
+    return (th, tr), hits, res
 
 
 # ------------------------------------------------------------------ device API (torch tensors)

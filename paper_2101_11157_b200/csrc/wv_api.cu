@@ -81,22 +81,30 @@ static int set_err(int code, const char *fmt, ...) {
 // env vars WV_VARIANT0/1/2 (index into this table) for benchmarking; defaults below.
 typedef void (*ResKern)(const Rec *, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, ulonglong2 *,
                         unsigned long long *, uint32_t);
-struct Variant { const char *name; int cls; ResKern fn; };
+typedef void (*LaneKern)(const Rec *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
+                         uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *);
+struct Variant { const char *name; int cls; ResKern fn; LaneKern lane; };
 static const Variant kVariants[] = {
-    {"c0 int s1/1", 0, residue_kernel<Mont32, 0, 0, 1, 1>},
-    {"c0 int s2/2", 0, residue_kernel<Mont32, 0, 0, 2, 2>},
-    {"c0 int s3/2", 0, residue_kernel<Mont32, 0, 0, 3, 2>},
-    {"c0 int s3/3", 0, residue_kernel<Mont32, 0, 0, 3, 3>},
-    {"c0 fp s1/1", 0, residue_kernel<Mont32, 0, 1, 1, 1>},
-    {"c1 fp s1/1", 1, residue_kernel<Mont64, 1, 1, 1, 1>},
-    {"c1 fp s2/2", 1, residue_kernel<Mont64, 1, 1, 2, 2>},
-    {"c1 int s1/1", 1, residue_kernel<Mont64, 2, 0, 1, 1>},
-    {"c2 int s1/1", 2, residue_kernel<Mont64, 2, 0, 1, 1>},
-    {"c2 int s2/2", 2, residue_kernel<Mont64, 2, 0, 2, 2>},
+    {"c0 int s1/1", 0, residue_kernel<Mont32, 0, 0, 1, 1>, nullptr},
+    {"c0 int s2/2", 0, residue_kernel<Mont32, 0, 0, 2, 2>, nullptr},
+    {"c0 int s3/2", 0, residue_kernel<Mont32, 0, 0, 3, 2>, nullptr},
+    {"c0 int s3/3", 0, residue_kernel<Mont32, 0, 0, 3, 3>, nullptr},
+    {"c0 fp s1/1", 0, residue_kernel<Mont32, 0, 1, 1, 1>, nullptr},
+    {"c1 fp s1/1", 1, residue_kernel<Mont64, 1, 1, 1, 1>, nullptr},
+    {"c1 fp s2/2", 1, residue_kernel<Mont64, 1, 1, 2, 2>, nullptr},
+    {"c1 int s1/1", 1, residue_kernel<Mont64, 2, 0, 1, 1>, nullptr},
+    {"c2 int s1/1", 2, residue_kernel<Mont64, 2, 0, 1, 1>, nullptr},
+    {"c2 int s2/2", 2, residue_kernel<Mont64, 2, 0, 2, 2>, nullptr},
+    {"c0 lane int", 0, nullptr, residue_lane_kernel<Mont32, 0, 0>},   // lane mode (sorted lists)
+    {"c0 lane fp", 0, nullptr, residue_lane_kernel<Mont32, 0, 1>},
+    {"c0 int s1/1 pairs", 0, residue_kernel<Mont32, 0, 0, 1, 1, true>, nullptr},
+    {"c0 int s2/2 pairs", 0, residue_kernel<Mont32, 0, 0, 2, 2, true>, nullptr},
+    {"c2 int s1/1 pairs", 2, residue_kernel<Mont64, 2, 0, 1, 1, true>, nullptr},
 };
 static const int NVAR = sizeof kVariants / sizeof kVariants[0];
-static const int kDefaultVariant[3] = {1, 6, 8};   // measured best (scripts/variant_sweep.py)
-static int g_variant[3] = {1, 6, 8};               // per class
+static const int kDefaultVariant[3] = {13, 6, 8};  // measured best (scripts/variant_sweep.py)
+static int g_variant[3] = {13, 6, 8};              // per class
+static const int kChunkFallback0 = 13;             // class-0 chunk variant when lane mode is unusable
 static void read_variant_env() {
     static bool done = false;
     if (done) return;
@@ -136,7 +144,10 @@ static int ctx_get(DevCtx **out) {
         c.sms = prop.multiProcessorCount;
         CK(cudaMemcpyToSymbol(c_cong, h_cong, sizeof h_cong));
         for (int v = 0; v < NVAR; v++) {
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[v], kVariants[v].fn, RES_THREADS, 0));
+            if (kVariants[v].fn)
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[v], kVariants[v].fn, RES_THREADS, 0));
+            else
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[v], kVariants[v].lane, RES_THREADS, 0));
             if (c.occ[v] < 1) c.occ[v] = 1;
         }
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
@@ -215,7 +226,8 @@ struct Layout {
     uint64_t prime_cap, K;
     // offsets into the workspace
     size_t o_misc, o_bitmap, o_segcnt, o_segoff, o_tiles, o_base1, o_recs, o_nch, o_start, o_part,
-           o_flags, o_pos, o_kb, total;
+           o_flags, o_pos, o_kb, o_gq, o_gstart, total;
+    uint64_t ngt;           // lane-mode group-tests: ceil(prime_cap / 32) * ntests
     uint64_t tiles_n;
 };
 
@@ -226,8 +238,12 @@ static void layout_tail(Layout &L) {
     L.o_start = o; o += al((L.K + 1) * 8);
     L.o_part = o;  o += al(PART_BUDGET * sizeof(ulonglong2));
     L.o_kb = o;    o += al(2 * (L.K * CAP_CHUNKS / (PART_BUDGET / 2) + 4) * 8);
+    L.ngt = (L.prime_cap + 31) / 32 * L.ntests;
+    L.o_gq = o;     o += al((L.ngt + 1) * 8);
+    L.o_gstart = o; o += al((L.ngt + 1) * 8);
     uint64_t t = ntiles(L.K + 1);
     if (ntiles(L.prime_cap) > t) t = ntiles(L.prime_cap);
+    if (ntiles(L.ngt + 1) > t) t = ntiles(L.ngt + 1);
     if (L.tiles_n < t) L.tiles_n = t;
     L.o_tiles = o; o += al(L.tiles_n * 8);
     L.total = o;
@@ -356,21 +372,39 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     ulonglong2 *part = (ulonglong2 *)WS(ws, L.o_part);
     uint64_t *kb = (uint64_t *)WS(ws, L.o_kb);
     uint64_t *tiles = (uint64_t *)WS(ws, L.o_tiles);
+    uint64_t *gq = (uint64_t *)WS(ws, L.o_gq);
+    uint64_t *gstart = (uint64_t *)WS(ws, L.o_gstart);
+    read_variant_env();
+    int var0 = g_variant[0];
+    bool lane = sorted && kVariants[var0].lane != nullptr;
+    if (!lane && kVariants[var0].lane) var0 = kChunkFallback0;
     const unsigned grid_plan = (unsigned)((K + 255) / 256 < (uint64_t)c->sms * 32 ? (K + 255) / 256 : c->sms * 32);
-    if (K > 0) {
-        LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs, nch,
-               (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
-               (unsigned long long *)(misc + M_TERMS));
-    }
-    TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
-    LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
-    uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, (split g32, k64)
+    uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
     uint64_t hs[4], ht[3];
-    CK(cudaMemcpyAsync(ht, misc + M_TERMS, 24, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 32, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    for (int attempt = 0; attempt < 2; attempt++) {
+        if (attempt == 1) {       // lane mode needs more partial pairs than one batch: redo in chunk mode
+            lane = false;
+            var0 = kChunkFallback0;
+            CK(cudaMemsetAsync(misc + M_ERR, 0, 8, st));
+            CK(cudaMemsetAsync(misc + M_FIRST64, 0xff, 16, st));
+            CK(cudaMemsetAsync(misc + M_TERMS, 0, 24, st));
+        }
+        if (K > 0) {
+            LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
+                   nch, (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
+                   (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr);
+        }
+        TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
+        if (lane) TRY(scan_excl<uint64_t>(gq, L.ngt, gstart, gstart + L.ngt, tiles, st));
+        LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
+        CK(cudaMemcpyAsync(ht, misc + M_TERMS, 24, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
+        if (lane) CK(cudaMemcpyAsync(&h[3], gstart + L.ngt, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 32, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!lane || h[2] <= PART_BUDGET) break;
+    }
     const uint64_t n = n_dev ? h[0] : n_host;
     if (n_primes_out) *n_primes_out = n;
     if ((int)h[1] != 0) return set_err(WV_EINVAL, "schedule chose a congruence not valid for some prime");
@@ -388,7 +422,6 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     // class boundaries (sorted input): items [0,gb[1]) class 0, [gb[1],gb[2]) class 1, [gb[2],G) class 2
     const uint64_t gb[4] = {0, sorted ? hs[0] : 0, sorted ? hs[2] : 0, G};
     const uint64_t kbd[4] = {0, sorted ? hs[1] : 0, sorted ? hs[3] : 0, K};
-    read_variant_env();
     // batches of <= PART_BUDGET partial pairs, cut at record boundaries
     std::vector<uint64_t> hk, hg;
     if (G <= PART_BUDGET) {
@@ -410,7 +443,16 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         // 32-bit records: items [glo, min(ghi, g32)); 64-bit: [max(glo, g32), ghi)
         // per class: items [max(glo, gb[c]), min(ghi, gb[c+1])) of records [max(klo,kbd[c]), min(khi,kbd[c+1]));
         // unsorted input: every class kernel scans the whole batch and skips the other classes' records
+        if (lane && h[3] > 0) {     // lane mode for class 0 (single batch guaranteed above)
+            CK(cudaMemsetAsync(misc + M_CNT, 0, 8, st));
+            EvPair ev{nullptr, nullptr, 0};
+            if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
+            LAUNCH(kVariants[var0].lane, c->sms * c->occ[var0], RES_THREADS, st, recs, start, gstart, gq, L.ngt, h[3],
+                   L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT));
+            if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
+        }
         for (int cls = 0; cls < 3; cls++) {
+            if (cls == 0 && lane) continue;
             uint64_t a_ = glo, b_ = ghi, ka = klo, kz = khi;
             if (sorted) {
                 a_ = glo > gb[cls] ? glo : gb[cls];
@@ -423,13 +465,13 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             EvPair ev{nullptr, nullptr, cls};
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
             unsigned long long *cnt = (unsigned long long *)(misc + M_CNT + cls);
-            const int var = g_variant[cls];
+            const int var = cls == 0 ? var0 : g_variant[cls];
             const unsigned grid = c->sms * c->occ[var];
             LAUNCH(kVariants[var].fn, grid, RES_THREADS, st, recs, start, ka, kz, a_, b_, glo, part, cnt, 1u << cls);
             if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         const uint64_t nrec = khi - klo;
-        uint64_t fb = (nrec * 32 + 255) / 256;
+        uint64_t fb = (nrec + 255) / 256;
         if (fb > (uint64_t)c->sms * 16) fb = (uint64_t)c->sms * 16;
         LAUNCH(finalize_kernel, (unsigned)fb, 256, st, recs, start, klo, khi, glo, part, res_w, res_v);
     }

@@ -46,6 +46,14 @@ struct Mont32 {
         uint32_t s = a + b;                     // < 4p < 2^32
         return min(s, s - p2);
     }
+    // (a b + c d) R^{-1} mod p in [0, 2p) with one REDC: a, b, c, d < 2p, so
+    // T < 8p^2 and T + m p < 2^63 + 2^62; the REDC output is < 3p.
+    __device__ __forceinline__ uint32_t mul2add(uint32_t a, uint32_t b, uint32_t c, uint32_t d) const {
+        uint64_t T = (uint64_t)a * b + (uint64_t)c * d;
+        uint32_t m = (uint32_t)T * pinv;
+        uint32_t t = (uint32_t)((T + (uint64_t)m * p) >> 32);
+        return min(t, t - p2);
+    }
     __device__ __forceinline__ uint32_t to(uint64_t x) const { return mul((uint32_t)(x % p), r2); }
     __device__ __forceinline__ uint64_t canon(uint32_t x) const {  // Montgomery -> [0, p)
         uint32_t r = mul(x, 1u);                // <= p
@@ -83,6 +91,10 @@ struct Mont64 {
     __device__ __forceinline__ uint64_t add(uint64_t a, uint64_t b) const {
         uint64_t s = a + b;
         return min(s, s - p2);
+    }
+    // (a b + c d) R^{-1} mod p: two REDCs (a 128-bit double product would not fit the lazy bound)
+    __device__ __forceinline__ uint64_t mul2add(uint64_t a, uint64_t b, uint64_t c, uint64_t d) const {
+        return add(mul(a, b), mul(c, d));
     }
     __device__ __forceinline__ uint64_t to(uint64_t x) const { return mul(x % p, r2); }
     __device__ __forceinline__ uint64_t canon(uint64_t x) const {

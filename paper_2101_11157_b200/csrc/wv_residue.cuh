@@ -54,6 +54,8 @@ struct Sched {              // default schedule + overrides
 
 constexpr uint32_t CAP_CHUNKS = 1024;   // target max chunks per record
 constexpr uint32_t LMIN = 4096;         // min terms per lane in a full chunk
+constexpr uint64_t LANE_SLICE = 8192;   // lane mode: target terms per lane per slice
+constexpr uint64_t LANE_QMAX = 128;     // lane mode: max slices per record
 constexpr uint64_t WIDTH32_MAX = 1ull << 30;  // Mont32 (lazy, fused) needs p < 2^30
 constexpr uint64_t FP64_MAX = 1ull << 44;     // ModD (FP64 engine) needs p < 2^44
 __host__ __device__ __forceinline__ int prime_class(uint64_t p) { return p < WIDTH32_MAX ? 0 : (p < FP64_MAX ? 1 : 2); }
@@ -74,6 +76,16 @@ __host__ __device__ __forceinline__ int schedule(const Sched &s, uint64_t p, int
 
 // first and count of integers s with x p < s < y p  (x = xn/xd, y = yn/yd), exact.
 __device__ __forceinline__ void sum_bounds(uint64_t p, const Term &t, uint64_t *first, uint64_t *count) {
+    if (p < (1ull << 32)) {                 // 32-bit division (den <= 2160, num < den)
+        const uint32_t p32 = (uint32_t)p;
+        const uint32_t qx = p32 / t.xd, rx = p32 % t.xd, qy = p32 / t.yd, ry = p32 % t.yd;
+        const uint64_t fl = (uint64_t)t.xn * qx + (t.xn * rx) / t.xd;
+        const uint64_t ce = (uint64_t)t.yn * qy + (t.yn * ry + t.yd - 1) / t.yd;
+        const uint64_t f = fl + 1, l = ce - 1;
+        *first = f;
+        *count = l >= f ? l - f + 1 : 0;
+        return;
+    }
     uint64_t qx = p / t.xd, rx = p % t.xd;
     uint64_t fl = (uint64_t)t.xn * qx + ((uint64_t)t.xn * rx) / t.xd;      // floor(x p)
     uint64_t qy = p / t.yd, ry = p % t.yd;
@@ -89,7 +101,7 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
                             uint64_t n_primes_host, uint64_t kmax, uint32_t mode, Sched sched,
                             Rec *__restrict__ recs, uint64_t *__restrict__ nchunks,
                             unsigned long long *__restrict__ first64, int *__restrict__ err,
-                            unsigned long long *__restrict__ terms) {
+                            unsigned long long *__restrict__ terms, uint64_t *__restrict__ gq) {
     const uint32_t ntests = (mode == 3) ? 2 : 1;
     const uint64_t n = n_primes_dev ? *n_primes_dev : n_primes_host;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kmax;
@@ -114,7 +126,27 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         uint64_t L = (T + 32ull * CAP_CHUNKS - 1) / (32ull * CAP_CHUNKS);
         if (L < LMIN) L = LMIN;
         if (L > 0x40000000ull) L = 0x40000000ull;
-        const uint64_t nc = (T + 32 * L - 1) / (32 * L);
+        uint64_t nc = (T + 32 * L - 1) / (32 * L);
+        if (gq && p < WIDTH32_MAX) {
+            // lane mode: group g = 32 consecutive primes of this test, one per lane; Q slices,
+            // Q fixed by the group's last prime so all 32 records agree (T grows with p)
+            const uint64_t g = i / 32;
+            const uint64_t il = (32 * g + 31 < n) ? 32 * g + 31 : n - 1;
+            const uint64_t pl = primes[il];
+            const int cl = schedule(sched, pl, (int)test);
+            uint64_t Tl = 0;
+            if (cl >= 0 && cl < NCONG)
+                for (uint32_t jj = 0; jj < c_cong[cl].m; jj++) {
+                    uint64_t f, cnt;
+                    sum_bounds(pl, c_cong[cl].t[jj], &f, &cnt);
+                    Tl += cnt;
+                }
+            uint64_t Q = (Tl + LANE_SLICE - 1) / LANE_SLICE;
+            if (Q < 1) Q = 1;
+            if (Q > LANE_QMAX) Q = LANE_QMAX;
+            nc = Q;
+            if (i == 32 * g) gq[g * ntests + (mode == 3 ? test : 0)] = Q;
+        }
         Rec r;
         r.p = p; r.T = T; r.cid = (uint32_t)cid; r.L = (uint32_t)L; r.idx = (uint32_t)i; r.test = test;
         recs[k] = r;
@@ -122,6 +154,15 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         if (p >= WIDTH32_MAX && nc > 0) atomicMin(first64, (unsigned long long)k);
         if (p >= FP64_MAX && nc > 0) atomicMin(first64 + 1, (unsigned long long)k);
         atomicAdd(&terms[prime_class(p)], (unsigned long long)T);
+    }
+    // lane-mode groups whose first prime is not class 0 (or beyond n) get Q = 0
+    if (gq) {
+        const uint64_t ngt = ((kmax / ntests + 31) / 32) * ntests;
+        for (uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gt < ngt;
+             gt += (uint64_t)gridDim.x * blockDim.x) {
+            const uint64_t i0 = (gt / ntests) * 32;
+            if (i0 >= n || primes[i0] >= WIDTH32_MAX) gq[gt] = 0;
+        }
     }
 }
 
@@ -177,6 +218,31 @@ struct Run {
         d1 = mo.add(d1, d2);
         if (E == 3) d2 = mo.add(d2, d3);
     }
+    // two terms at once: 1/u1 + 1/u2 = (u1 + u2) / (u1 u2), so with D = u1 u2, N = u1 + u2:
+    //   a1 <- a1 D + a0 N  (one REDC for both products),  a0 <- a0 D
+    // 5 Montgomery-product halves instead of 6 for the pair (PAIRS engines only).
+    __device__ __forceinline__ void step2(const M &mo, const ModD &) {
+        const W u2 = mo.add(u, d1);
+        d1 = mo.add(d1, d2);
+        if (E == 3) d2 = mo.add(d2, d3);
+        const W N = mo.add(u, u2);
+        const W D = mo.mul(u, u2);
+        u = mo.add(u2, d1);
+        d1 = mo.add(d1, d2);
+        if (E == 3) d2 = mo.add(d2, d3);
+        a1 = mo.mul2add(a1, D, a0, N);
+        a0 = mo.mul(a0, D);
+    }
+    // a step whose (a0, a1) update only lands on lanes with act (the differences always advance)
+    __device__ __forceinline__ void step_masked(const M &mo, const ModD &, bool act) {
+        const W n1 = mo.muladd(a1, u, a0);
+        const W n0 = mo.mul(a0, u);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
+        u = mo.add(u, d1);
+        d1 = mo.add(d1, d2);
+        if (E == 3) d2 = mo.add(d2, d3);
+    }
     __device__ __forceinline__ void reduce(const ModD &) {}
     __device__ __forceinline__ void result(const M &, const ModD &, W &c0, W &c1) const { c0 = a0; c1 = a1; }
 };
@@ -204,6 +270,16 @@ struct RunD {
     __device__ __forceinline__ void step(const M &, const ModD &md) {
         a1 = __dadd_rn(md.mul(a1, u), a0);       // |a1| <= 2p
         a0 = md.mul(a0, u);                      // |a0| <= p
+        u = __dadd_rn(u, d1);
+        d1 = __dadd_rn(d1, d2);
+        if (E == 3) d2 = __dadd_rn(d2, 6.0);
+    }
+    __device__ __forceinline__ void step2(const M &mo, const ModD &md) { step(mo, md); step(mo, md); }
+    __device__ __forceinline__ void step_masked(const M &, const ModD &md, bool act) {
+        const double n1 = __dadd_rn(md.mul(a1, u), a0);
+        const double n0 = md.mul(a0, u);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
         u = __dadd_rn(u, d1);
         d1 = __dadd_rn(d1, d2);
         if (E == 3) d2 = __dadd_rn(d2, 6.0);
@@ -238,7 +314,7 @@ constexpr int RES_WARPS = RES_THREADS / 32;
 // re-seed u and its differences) runs where a run ended.  Finished streams keep
 // stepping on dead state (ignored).  The FP64 engine range-reduces its u (and
 // d1) every rb terms, counted warp-uniformly.
-template <class M, class R, int E, int S>
+template <class M, class R, int E, int S, bool PAIRS>
 __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Cong &cg, uint64_t p,
                                           const uint64_t *first, const uint64_t *cum, uint64_t t0, uint64_t t1,
                                           typename M::W &C0, typename M::W &C1) {
@@ -275,12 +351,23 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Con
         while (left) {
             const uint32_t kk = left < rb - since ? left : rb - since;
             uint32_t i = 0;
-            #pragma unroll 1
-            for (; i + 4 <= kk; i += 4) {
-                #pragma unroll
-                for (int u = 0; u < 4; u++) {
+            if (PAIRS) {
+                #pragma unroll 1
+                for (; i + 4 <= kk; i += 4) {
                     #pragma unroll
-                    for (int s_ = 0; s_ < S; s_++) run[s_].step(mo, md);
+                    for (int u = 0; u < 2; u++) {
+                        #pragma unroll
+                        for (int s_ = 0; s_ < S; s_++) run[s_].step2(mo, md);
+                    }
+                }
+            } else {
+                #pragma unroll 1
+                for (; i + 4 <= kk; i += 4) {
+                    #pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        #pragma unroll
+                        for (int s_ = 0; s_ < S; s_++) run[s_].step(mo, md);
+                    }
                 }
             }
             for (; i < kk; i++) {
@@ -324,7 +411,7 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Con
 
 // ENGINE: 0 = IMAD runs, 1 = FP64 runs;  S = streams per lane (E = 2 / E = 3 sums)
 // Persistent: each warp pulls items g in [g_lo, g_hi) from *counter (reset to 0 before launch).
-template <class M, int CLASS, int ENGINE, int S2, int S3>
+template <class M, int CLASS, int ENGINE, int S2, int S3, bool PAIRS = false>
 __global__ void __launch_bounds__(RES_THREADS)
 residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
                uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
@@ -372,11 +459,11 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         ModD md;
         if (ENGINE == 1) {
             md.init(r.p);
-            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
-            else lane_work<M, RunD<M, 2>, 2, S2>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3, false>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            else lane_work<M, RunD<M, 2>, 2, S2, false>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
         } else {
-            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
-            else lane_work<M, Run<M, 2>, 2, S2>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3, PAIRS>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            else lane_work<M, Run<M, 2>, 2, S2, PAIRS>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
         }
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -389,43 +476,136 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
     }
 }
 
-// One warp per record in [klo, khi): merge the record's chunk pairs, invert, store.
+
+// ---------------------------------------------------------------- lane mode
+// Lane mode (sorted prime lists, class 0): a warp item is (group of 32 consecutive
+// primes of one test, slice q of Q).  Lane l owns record (32g + l, test) and
+// evaluates slice q of every sum of its congruence: for sum j with n_j terms the
+// slice is [floor(q n_j / Q), floor((q+1) n_j / Q)).  Neighbouring primes share
+// the congruence and have nearly equal n_j, so each sum is one warp-uniform loop:
+// min-count unpredicated steps, then a short predicated tail up to the max count.
+// One record per lane removes the per-boundary lockstep breaks of chunk mode.
+template <class M, class R, int E>
+__device__ __forceinline__ void lane_slice_work(const M &mo, const ModD &md, const Cong &cg, uint64_t p, bool valid,
+                                                uint64_t q, uint64_t Q, typename M::W &C0, typename M::W &C1) {
+    using W = typename M::W;
+    const uint32_t m = valid ? cg.m : 0;
+    const uint32_t mmax = __reduce_max_sync(0xffffffffu, m);
+    uint32_t rb = R::kFP ? (E == 3 ? md.rb3 : md.rb2) : 0xffffffffu;
+    if (R::kFP) rb = __reduce_min_sync(0xffffffffu, valid ? rb : 0xffffffffu);
+    R run;
+    for (uint32_t j = 0; j < mmax; j++) {
+        uint32_t cnt = 0;
+        uint64_t s0 = 1;
+        if (j < m) {
+            uint64_t f, n;
+            sum_bounds(p, cg.t[j], &f, &n);
+            const uint64_t a = n * q / Q, b = n * (q + 1) / Q;
+            cnt = (uint32_t)(b - a);
+            s0 = f + a;
+        }
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
+        if (kmax == 0) continue;
+        const uint32_t kmin = __reduce_min_sync(0xffffffffu, cnt ? cnt : 0xffffffffu);
+        run.setup(mo, md, s0);
+        uint32_t i = 0, since = 0;
+        while (i < kmin) {
+            const uint32_t kk0 = kmin - i;
+            const uint32_t kk = kk0 < rb - since ? kk0 : rb - since;
+            uint32_t x = 0;
+            #pragma unroll 1
+            for (; x + 4 <= kk; x += 4) {
+                run.step(mo, md); run.step(mo, md); run.step(mo, md); run.step(mo, md);
+            }
+            for (; x < kk; x++) run.step(mo, md);
+            i += kk;
+            if (R::kFP) {
+                since += kk;
+                if (since == rb) { run.reduce(md); since = 0; }
+            }
+        }
+        for (; i < kmax; i++) {
+            run.step_masked(mo, md, i < cnt);
+            if (R::kFP && ++since == rb) { run.reduce(md); since = 0; }
+        }
+        if (cnt) {
+            W c0, c1;
+            run.result(mo, md, c0, c1);
+            c1 = mo.mul(c1, mo.mul((W)smod(cg.t[j].a, p), mo.r2));   // fold a_j
+            combine(mo, C0, C1, c0, c1);
+        }
+    }
+}
+
+// items it in [0, nitems) processed largest-first (groups ascend in p);
+// gstart = exclusive scan of gq over group-tests; start = per-record partial slots.
+template <class M, int CLASS, int ENGINE>
+__global__ void __launch_bounds__(RES_THREADS)
+residue_lane_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
+                    const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
+                    uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
+                    ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter) {
+    using W = typename M::W;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long it = 0;
+        if (lane == 0) it = atomicAdd(counter, 1ull);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) break;
+        const uint64_t item = nitems - 1 - it;
+        const uint64_t gt = find_rec(gstart, 0, ngt, item);
+        const uint64_t q = item - gstart[gt], Q = gq[gt];
+        const uint64_t g = gt / ntests, t = gt % ntests;
+        const uint64_t k = (32 * g + lane) * ntests + t;
+        Rec r;
+        r.p = 0;
+        if (k < K) r = recs[k];
+        const bool valid = r.p != 0 && prime_class(r.p) == CLASS;
+        const Cong &cg = c_cong[valid ? r.cid : 0];
+        M mo;
+        mo.init(valid ? r.p : 7);
+        W C0 = mo.r1, C1 = 0;
+        ModD md;
+        const uint32_t e = __reduce_max_sync(0xffffffffu, valid ? cg.e : 0);   // one test per item
+        if (ENGINE == 1) {
+            md.init(valid ? r.p : 7);
+            if (e == 3) lane_slice_work<M, RunD<M, 3>, 3>(mo, md, cg, r.p, valid, q, Q, C0, C1);
+            else lane_slice_work<M, RunD<M, 2>, 2>(mo, md, cg, r.p, valid, q, Q, C0, C1);
+        } else {
+            if (e == 3) lane_slice_work<M, Run<M, 3>, 3>(mo, md, cg, r.p, valid, q, Q, C0, C1);
+            else lane_slice_work<M, Run<M, 2>, 2>(mo, md, cg, r.p, valid, q, Q, C0, C1);
+        }
+        if (valid) partials[start[k] + q - part_base] = make_ulonglong2((unsigned long long)C0, (unsigned long long)C1);
+    }
+}
+
+// One thread per record in [klo, khi): merge the record's chunk pairs, invert, store.
 template <class M>
 __device__ __forceinline__ void finalize_one(const Rec &r, const uint64_t *start, uint64_t k, uint64_t part_base,
                                              const ulonglong2 *partials, uint64_t *res_w, uint64_t *res_v) {
     using W = typename M::W;
-    const int lane = threadIdx.x & 31;
     M mo;
     mo.init(r.p);
     W C0 = mo.r1, C1 = 0;
     const uint64_t s = start[k], e = start[k + 1];
-    for (uint64_t g = s + lane; g < e; g += 32) {
-        ulonglong2 v = partials[g - part_base];
+    for (uint64_t g = s; g < e; g++) {
+        const ulonglong2 v = partials[g - part_base];
         combine(mo, C0, C1, (W)v.x, (W)v.y);
     }
-    #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        W o0 = __shfl_xor_sync(0xffffffffu, C0, o);
-        W o1 = __shfl_xor_sync(0xffffffffu, C1, o);
-        combine(mo, C0, C1, o0, o1);
-    }
-    if (lane == 0) {
-        const Cong &cg = c_cong[r.cid];
-        const W Lm = mo.to(smod(cg.L, r.p));
-        const W den = mo.mul(C0, Lm);
-        const W X = mo.mul(C1, mont_inv(mo, den));
-        const uint64_t x = mo.canon(X);
-        if (r.test == 0) res_w[r.idx] = x; else res_v[r.idx] = x;
-    }
+    const Cong &cg = c_cong[r.cid];
+    const W Lm = mo.mul((W)smod(cg.L, r.p), mo.r2);
+    const W den = mo.mul(C0, Lm);
+    const W X = mo.mul(C1, mont_inv(mo, den));
+    const uint64_t x = mo.canon(X);
+    if (r.test == 0) res_w[r.idx] = x; else res_v[r.idx] = x;
 }
 
 __global__ void finalize_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                                 uint64_t klo, uint64_t khi, uint64_t part_base,
                                 const ulonglong2 *__restrict__ partials,
                                 uint64_t *__restrict__ res_w, uint64_t *__restrict__ res_v) {
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t k = klo + warp; k < khi; k += nwarps) {
+    for (uint64_t k = klo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < khi;
+         k += (uint64_t)gridDim.x * blockDim.x) {
         const Rec r = recs[k];
         if (r.p == 0) continue;                     // padding record (beyond n primes)
         if (r.p < WIDTH32_MAX) finalize_one<Mont32>(r, start, k, part_base, partials, res_w, res_v);
