@@ -135,6 +135,21 @@ int wv_residues_device(const uint64_t *d_primes, size_t n, uint32_t mode,
 int wv_sieve_device(uint64_t lo, uint64_t hi, uint64_t *d_primes, size_t cap, size_t *n,
                     void *d_workspace, size_t workspace_bytes, void *stream);
 
+/* Near misses and histograms.
+ * For residues already on the device (e.g. the outputs of wv_search_device):
+ *   symmetric residue <r>_p in (-p/2, p/2];
+ *   near miss: |<r>_p| < bound  -> d_out[] entries (unordered), *n_out = count
+ *     (if the count exceeds cap, only cap entries are written and WV_ENOSPC
+ *      is returned with *n_out = the full count);
+ *   histogram: 2000 equal bins of <r>_p / p over (-1/2, 1/2],
+ *     bin = floor(2000 (<r>_p + p/2) / p) computed exactly; d_hist_w/v[2000]
+ *     uint64 counts are ADDED to (zero them first); either may be NULL.
+ * Tests whose residue array holds WV_RES_NONE are skipped.  Synchronises the stream. */
+typedef struct { uint64_t p; int64_t symres; uint32_t test; uint32_t reserved; } wv_nearmiss;  /* test 1=W, 2=V */
+int wv_near_misses_device(const uint64_t *d_primes, const uint64_t *d_res_w, const uint64_t *d_res_v, size_t n,
+                          uint64_t bound, wv_nearmiss *d_out, size_t cap, size_t *n_out,
+                          uint64_t *d_hist_w, uint64_t *d_hist_v, void *d_workspace, void *stream);
+
 /* wv_prime_count: number of primes q with max(lo,5) <= q < hi, counted by the
  * same segmented sieve without materialising them (used to pin the sieve to
  * the paper's counts).  Device scratch is internal. */

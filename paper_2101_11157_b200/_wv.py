@@ -22,6 +22,7 @@ HIT_W, HIT_V = 1, 2
 
 HIT_DTYPE = np.dtype([("p", "<u8"), ("flags", "<u4"), ("reserved", "<u4")])
 RES_DTYPE = np.dtype([("p", "<u8"), ("res_w", "<u8"), ("res_v", "<u8")])
+NEAR_DTYPE = np.dtype([("p", "<u8"), ("symres", "<i8"), ("test", "<u4"), ("reserved", "<u4")])
 
 
 class WVError(RuntimeError):
@@ -60,6 +61,7 @@ SIGNATURES = {
     "wv_residues_device": (_i, [_vp, _sz, _u32, _vp, _vp, _vp, _sz, _vp]),
     "wv_sieve_device": (_i, [_u64, _u64, _vp, _sz, _P(_sz), _vp, _sz, _vp]),
     "wv_prime_count": (_i, [_u64, _u64, _P(_u64)]),
+    "wv_near_misses_device": (_i, [_vp, _vp, _vp, _sz, _u64, _vp, _sz, _P(_sz), _vp, _vp, _vp, _vp]),
     "wv_shard_blocks": (_i, [_u64, _u64, _u32, _u32, _u64, _vp, _sz, _P(_sz), _P(_u64)]),
     "wv_checksum_term": (_u64, [_u64, _u64, _u64]),
     "wv_congruence_count": (_i, []),
@@ -200,6 +202,29 @@ class DeviceSearch:
 
     def checksum_int(self):
         return int(self.checksum.cpu().numpy().view(np.uint64)[0])
+
+    def near_misses(self, bound=50, histograms=True, cap=1 << 16):
+        """NEXT-1: near misses |<r>_p| < bound (sorted by p, test) and the
+        2000-bin histograms of <r>_p / p for W and V (numpy uint64[2000] each, zeros if not requested)."""
+        return near_misses_device(self.primes, self.res_w, self.res_v, self.n_primes, bound, histograms, cap)
+
+
+def near_misses_device(primes, res_w, res_v, n, bound=50, histograms=True, cap=1 << 16, stream=None):
+    """wv_near_misses_device on torch cuda tensors -> (near: NEAR_DTYPE sorted, hist_w, hist_v)."""
+    import torch
+    dev = primes.device
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    out = torch.empty(max(cap, 1) * 3, dtype=torch.int64, device=dev)        # NEAR_DTYPE = 24 bytes
+    hw = torch.zeros(2000, dtype=torch.int64, device=dev) if histograms else None
+    hv = torch.zeros(2000, dtype=torch.int64, device=dev) if histograms else None
+    cnt = ctypes.c_size_t()
+    _check(lib().wv_near_misses_device(_ptr(primes), _ptr(res_w), _ptr(res_v), n, bound, _ptr(out), cap,
+                                       ctypes.byref(cnt), _ptr(hw), _ptr(hv), None, ctypes.c_void_p(st.cuda_stream)))
+    raw = out[: 3 * cnt.value].cpu().numpy().view(np.uint8)
+    near = np.sort(np.frombuffer(raw.tobytes(), dtype=NEAR_DTYPE), order=["p", "test"])
+    z = np.zeros(2000, dtype=np.uint64)
+    return near, (hw.cpu().numpy().view(np.uint64) if hw is not None else z), \
+        (hv.cpu().numpy().view(np.uint64) if hv is not None else z)
 
 
 def residues_device(primes, mode=MODE_BOTH, stream=None):

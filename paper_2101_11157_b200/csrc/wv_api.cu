@@ -660,6 +660,39 @@ extern "C" int wv_sieve_device(uint64_t lo, uint64_t hi, uint64_t *d_primes, siz
     return WV_OK;
 }
 
+extern "C" int wv_near_misses_device(const uint64_t *d_primes, const uint64_t *d_res_w, const uint64_t *d_res_v,
+                                     size_t n, uint64_t bound, wv_nearmiss *d_out, size_t cap, size_t *n_out,
+                                     uint64_t *d_hist_w, uint64_t *d_hist_v, void *d_workspace, void *stream) {
+    static_assert(sizeof(wv_nearmiss) == sizeof(NearOut), "wv_nearmiss layout");
+    if (!d_primes || !d_res_w || !d_res_v) return set_err(WV_EINVAL, "null pointer");
+    DevCtx *c;
+    TRY(ctx_get(&c));
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long *cnt = (unsigned long long *)d_workspace;
+    if (!cnt) CK(cudaMallocAsync((void **)&cnt, 8, st));
+    int rc = WV_OK;
+    unsigned long long h = 0;
+    if (cudaMemsetAsync(cnt, 0, 8, st) != cudaSuccess) rc = set_err(WV_ECUDA, "memset");
+    if (rc == WV_OK && n > 0) {
+        unsigned g = (unsigned)((n + 255) / 256 < (uint64_t)c->sms * 16 ? (n + 255) / 256 : c->sms * 16);
+        nearmiss_kernel<<<g, 256, 0, st>>>(d_primes, n, d_res_w, d_res_v, bound, (NearOut *)d_out,
+                                           d_out ? cap : 0, cnt, (unsigned long long *)d_hist_w,
+                                           (unsigned long long *)d_hist_v);
+        g_launches.fetch_add(1);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = set_err(WV_ECUDA, "nearmiss_kernel: %s", cudaGetErrorString(e));
+    }
+    if (rc == WV_OK && cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = set_err(WV_ECUDA, "copy");
+    if (!d_workspace) cudaFreeAsync(cnt, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && rc == WV_OK) rc = set_err(WV_ECUDA, "near misses: %s", cudaGetErrorString(e));
+    if (rc != WV_OK) return rc;
+    if (n_out) *n_out = h;
+    if (h > cap) return set_err(WV_ENOSPC, "near-miss cap %zu < %llu", cap, (unsigned long long)h);
+    return WV_OK;
+}
+
 extern "C" int wv_prime_count(uint64_t lo, uint64_t hi, uint64_t *count) {
     Layout L;
     TRY(make_layout(lo, hi, 1, 0, 1, 0, L));

@@ -649,6 +649,38 @@ __global__ void flags_kernel(const uint64_t *__restrict__ primes, const uint64_t
 
 struct HitOut { uint64_t p; uint32_t flags; uint32_t reserved; };
 
+// ---------------------------------------------------------------- near misses / histograms (NEXT-1)
+struct NearOut { uint64_t p; int64_t symres; uint32_t test; uint32_t reserved; };
+
+__device__ __forceinline__ void near_one(uint64_t p, uint64_t r, uint32_t test, uint64_t bound, NearOut *out,
+                                         uint64_t cap, unsigned long long *count, unsigned long long *hist) {
+    if (r == ~0ull) return;
+    const bool neg = r > (p - 1) / 2;                    // <r> = r - p  if r > (p-1)/2
+    const uint64_t mag = neg ? p - r : r;
+    if (mag < bound) {
+        const unsigned long long slot = atomicAdd(count, 1ull);
+        if (slot < cap) out[slot] = NearOut{p, neg ? -(int64_t)mag : (int64_t)mag, test, 0};
+    }
+    if (hist) {
+        // x = 2<r> + p in [1, 2p-1];  bin = floor(1000 x / p)  in [0, 1999]
+        const uint64_t x = neg ? 2 * r - p : 2 * r + p;  // 2(r - p) + p = 2r - p for negative <r>
+        const unsigned __int128 num = (unsigned __int128)x * 1000u;
+        const uint32_t bin = (uint32_t)(num / p);
+        atomicAdd(&hist[bin < 2000 ? bin : 1999], 1ull);
+    }
+}
+
+__global__ void nearmiss_kernel(const uint64_t *__restrict__ primes, uint64_t n, const uint64_t *__restrict__ res_w,
+                                const uint64_t *__restrict__ res_v, uint64_t bound, NearOut *__restrict__ out,
+                                uint64_t cap, unsigned long long *__restrict__ count,
+                                unsigned long long *__restrict__ hist_w, unsigned long long *__restrict__ hist_v) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = primes[i];
+        near_one(p, res_w[i], 1, bound, out, cap, count, hist_w);
+        near_one(p, res_v[i], 2, bound, out, cap, count, hist_v);
+    }
+}
+
 __global__ void hits_scatter_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ n_dev,
                                     uint64_t kmax, const uint64_t *__restrict__ res_w,
                                     const uint64_t *__restrict__ res_v, const uint32_t *__restrict__ flags,

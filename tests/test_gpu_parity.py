@@ -294,3 +294,61 @@ def test_c4_c5_sampled_primes(wv, name):
     hits, res = wv.search(p0, p0 + 1, w.mode)
     assert res["p"].tolist() == [p0]
     assert (int(res["res_w"][0]) if w.mode & 1 else NONE) == int(gw[0])
+
+
+# ---------------------------------------------------------------- NEXT-1: near misses and histograms
+def _near_window(wv, lo, hi, mode, bound=50):
+    ds = wv.DeviceSearch(lo, hi, mode).run()
+    near, hw, hv = ds.near_misses(bound)
+    return ds, {(int(x["p"]), int(x["test"])): int(x["symres"]) for x in near}, hw, hv
+
+
+TABLE_WINDOWS = [
+    # (center, half-width, mode): Tables 2 and 3 are complete on (1e9, 6e10) / (1e9, 4e10),
+    # so a window around a listed prime must contain exactly the listed near misses
+    (2139716869, 100000, 1), (56604583391, 30000, 1), (1836806681, 100000, 2), (36830964851, 20000, 2),
+]
+
+
+@pytest.mark.parametrize("center,half,mode", TABLE_WINDOWS)
+def test_near_misses_match_complete_tables(wv, center, half, mode):
+    t2 = {int(r["p"]): int(r["symres_B"]) for r in _table("paper_table2_bernoulli.csv")}
+    t3 = {int(r["p"]): (int(r["symres_E"]), int(r["sign_exact"])) for r in _table("paper_table3_euler.csv")}
+    lo, hi = center - half, center + half
+    ds, near, hw, hv = _near_window(wv, lo, hi, mode)
+    if mode == 1:
+        want = {(p, 1): v for p, v in t2.items() if lo <= p < hi}
+    else:
+        want = {(p, 2): (v if ex else -v) for p, (v, ex) in t3.items() if lo <= p < hi}   # reading R2
+    assert near == want
+    hist = hw if mode == 1 else hv
+    assert int(hist.sum()) == ds.n_primes
+
+
+def test_near_misses_pin_window_and_c2_histograms(wv):
+    w = CONFIGS["pin_v"]
+    ds, near, hw, hv = _near_window(wv, w.lo, w.hi, w.mode)
+    assert near == {(1062232319, 2): 0}
+    w = CONFIGS["c2"]
+    ds, near, hw, hv = _near_window(wv, w.lo, w.hi, w.mode)
+    p = ds.primes_np().astype(object)
+    rw, rv = ds.res_np()
+    for res, hist, test in ((rw, hw, 1), (rv, hv, 2)):
+        r = res.astype(object)
+        sym = [int(a) - int(q) if int(a) > (int(q) - 1) // 2 else int(a) for a, q in zip(r, p)]
+        bins = np.bincount([(2 * s + int(q)) * 1000 // int(q) for s, q in zip(sym, p)], minlength=2000)
+        assert bins.tolist() == hist.tolist()
+        small = {(int(q), test): s for s, q in zip(sym, p) if abs(s) < 50}
+        assert {k: v for k, v in near.items() if k[1] == test} == small
+
+
+def test_c3_wolstenholme_near_misses_table2(wv):
+    """configs[2] window in W mode: Table 2 lists exactly 1025793739 (-9) and 1029113299 (-7) there
+    (table complete on (1e9, 6e10)); the histogram is flat (Fig. 1)."""
+    w = CONFIGS["c3"]
+    ds, near, hw, hv = _near_window(wv, w.lo, w.hi, 1)
+    assert near == {(1025793739, 1): -9, (1029113299, 1): -7}
+    n = ds.n_primes
+    exp = n / 2000
+    chi2 = float((((hw.astype(np.float64) - exp) ** 2) / exp).sum())
+    assert 1700 < chi2 < 2300            # 1999 degrees of freedom
