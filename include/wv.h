@@ -77,8 +77,11 @@ int wv_search(uint64_t lo, uint64_t hi, uint32_t mode,
 
 /* wv_search_shard: as wv_search, restricted to this shard's blocks.  [lo, hi)
  * is cut into blocks of `block` integers (0 = default: a power of two giving
- * every shard >= 32 blocks, at least 2^16); block b = [lo + b*block, ...)
- * belongs to shard b mod nshards (interleaved).  *checksum
+ * every shard >= 32 blocks, at least 2^15;
+ * any block must be a multiple of 2^15, the sieve segment); block b = [lo + b*block, ...)
+ * is dealt to shards in rounds of nshards, alternating direction ("snake"
+ * interleave: round j gives block j*N + s for even j and j*N + N-1-s for odd j
+ * to shard s), which balances the growth of per-prime work with p.  *checksum
  * receives this shard's order-independent 64-bit checksum (wv_checksum_term
  * summed mod 2^64), so shard checksums add up to the unsharded one.
  * checksum may be NULL. */

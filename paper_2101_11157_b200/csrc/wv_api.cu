@@ -159,7 +159,7 @@ static int ctx_get(DevCtx **out) {
         const uint32_t nboot = sizeof h_boot / sizeof h_boot[0];
         uint32_t *d_boot, *d_bitmap;
         uint64_t *d_cnt, *d_off, *d_tiles;
-        const uint64_t nseg = BASE0_HI / SIEVE_SPAN;  // 1 segment for [0, 65536)
+        const uint64_t nseg = BASE0_HI / SIEVE_SPAN;  // segments of [0, 65536)
         const uint64_t nseg1 = nseg > 0 ? nseg : 1;
         CK(cudaMalloc(&d_boot, sizeof h_boot));
         CK(cudaMalloc(&d_bitmap, nseg1 * SIEVE_WORDS * 4));
@@ -167,17 +167,17 @@ static int ctx_get(DevCtx **out) {
         CK(cudaMalloc(&d_off, (nseg1 + 1) * 8));
         CK(cudaMalloc(&d_tiles, 64));
         CK(cudaMemcpy(d_boot, h_boot, sizeof h_boot, cudaMemcpyHostToDevice));
-        SegMap m{0, BASE0_HI, SIEVE_SPAN, 0, 1, 1, 3};
+        SegMap m{0, BASE0_HI, BASE0_HI, 0, 1, BASE0_HI / SIEVE_SPAN, 3};
         cudaStream_t st = c.stream;
-        LAUNCH(sieve_segments_kernel, 1, SIEVE_THREADS, st, m, d_boot, nboot, nullptr, d_bitmap, d_cnt);
-        LAUNCH(scan_tile_totals<uint64_t>, 1, SCAN_THREADS, st, d_cnt, (uint64_t)1, d_tiles);
-        LAUNCH(scan_tiles_single, 1, SCAN_THREADS, st, d_tiles, (uint64_t)1, d_off + 1);
-        LAUNCH(scan_tile_apply<uint64_t>, 1, SCAN_THREADS, st, d_cnt, (uint64_t)1, d_tiles, d_off);
+        LAUNCH(sieve_segments_kernel, (unsigned)nseg1, SIEVE_THREADS, st, m, d_boot, nboot, nullptr, d_bitmap, d_cnt);
+        LAUNCH(scan_tile_totals<uint64_t>, 1, SCAN_THREADS, st, d_cnt, nseg1, d_tiles);
+        LAUNCH(scan_tiles_single, 1, SCAN_THREADS, st, d_tiles, (uint64_t)1, d_off + nseg1);
+        LAUNCH(scan_tile_apply<uint64_t>, 1, SCAN_THREADS, st, d_cnt, nseg1, d_tiles, d_off);
         uint64_t nb = 0;
-        CK(cudaMemcpyAsync(&nb, d_off + 1, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&nb, d_off + nseg1, 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         CK(cudaMalloc(&c.d_base0, nb * 4));
-        LAUNCH(sieve_write_kernel<uint32_t>, 1, SIEVE_THREADS, st, m, d_bitmap, d_off, c.d_base0, nb);
+        LAUNCH(sieve_write_kernel<uint32_t>, (unsigned)nseg1, SIEVE_THREADS, st, m, d_bitmap, d_off, c.d_base0, nb);
         CK(cudaStreamSynchronize(st));
         c.nbase0 = (uint32_t)nb;
         cudaFree(d_boot); cudaFree(d_bitmap); cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_tiles);
@@ -272,14 +272,16 @@ static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, 
     L.lo = lo; L.hi = hi; L.block = block; L.mode = mode; L.shard = shard; L.nshards = nshards;
     L.ntests = mode == 3 ? 2 : 1;
     const uint64_t nblocks = (width + block - 1) / block;
-    const uint64_t my_blocks = nblocks > shard ? (nblocks - shard + nshards - 1) / nshards : 0;
+    // blocks j of this shard: shard_block(j, shard, nshards) < nblocks (rounds of nshards, snake order)
+    uint64_t my_blocks = nblocks / nshards;
+    if (shard_block(my_blocks, shard, nshards) < nblocks) my_blocks++;
     const uint64_t spb = block / SIEVE_SPAN;
     L.map = SegMap{lo, hi, block, shard, nshards, spb, 5};
     L.nseg = my_blocks * spb;
     // primes in this shard: sum of per-block bounds
     uint64_t cap = 0;
     for (uint64_t j = 0; j < my_blocks; j++) {
-        uint64_t bs = lo + ((uint64_t)shard + j * nshards) * block;
+        uint64_t bs = lo + shard_block(j, shard, nshards) * block;
         uint64_t be = bs + block < hi ? bs + block : hi;
         cap += prime_bound(be - bs);
     }
@@ -810,7 +812,9 @@ extern "C" int wv_shard_blocks(uint64_t lo, uint64_t hi, uint32_t shard, uint32_
     TRY(make_layout(lo, hi, 1, shard, nshards, block, L));
     const uint64_t nblocks = (hi - lo + L.block - 1) / L.block;
     size_t k = 0;
-    for (uint64_t b = shard; b < nblocks; b += nshards) {
+    for (uint64_t j = 0;; j++) {
+        const uint64_t b = shard_block(j, shard, nshards);
+        if (b >= nblocks) break;
         const uint64_t a_ = lo + b * L.block, z = a_ + L.block < hi ? a_ + L.block : hi;
         if (z <= a_) continue;
         if (out && k < cap) { out[2 * k] = a_; out[2 * k + 1] = z; }

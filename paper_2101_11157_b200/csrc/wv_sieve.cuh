@@ -2,8 +2,8 @@
 //
 // The paper enumerates primes on the host ("for each prime p within its
 // assigned interval"); here the prime list is produced on the
-// device.  A window is a list of "segments" of 2^17 integers, each holding
-// 2^16 odd numbers as a 8 KB bitmap in shared memory (one CTA per segment).
+// device.  A window is a list of "segments" of 2^15 integers, each holding
+// 2^14 odd numbers as a 2 KB bitmap in shared memory (one CTA per segment).
 // Segments are laid out block-by-block for the interleaved shard partition
 // (block b of [lo,hi) belongs to shard b mod nshards).
 //
@@ -22,11 +22,19 @@
 
 namespace wv {
 
-constexpr int SIEVE_ODDS = 65536;                 // odd numbers per segment
-constexpr int SIEVE_SPAN = 2 * SIEVE_ODDS;        // integers per segment
-constexpr int SIEVE_WORDS = SIEVE_ODDS / 32;      // 2048
-constexpr int SIEVE_THREADS = 512;
+constexpr int SIEVE_ODDS = 16384;                 // odd numbers per segment
+constexpr int SIEVE_SPAN = 2 * SIEVE_ODDS;        // integers per segment (also the shard block granule)
+constexpr int SIEVE_WORDS = SIEVE_ODDS / 32;      // 512
+constexpr int SIEVE_THREADS = 256;
 constexpr uint32_t SIEVE_MED = 2048;              // phase-2 / phase-3 split
+
+// Block b of the window belongs to shard snake(b): blocks are dealt out in rounds of
+// nshards, alternating direction (0,1,..,N-1, N-1,..,1,0, ...), so that the linear
+// growth of per-prime work with p is balanced across shards.  The j-th block of
+// shard s is  j*N + (j even ? s : N-1-s).
+__host__ __device__ __forceinline__ uint64_t shard_block(uint64_t j, uint32_t s, uint32_t n) {
+    return j * n + ((j & 1) ? (uint64_t)(n - 1 - s) : (uint64_t)s);
+}
 
 struct SegMap {             // segment index -> integer range, for a shard of blocks
     uint64_t lo, hi;        // window [lo, hi)
@@ -37,7 +45,7 @@ struct SegMap {             // segment index -> integer range, for a shard of bl
 
     __host__ __device__ void range(uint64_t seg, uint64_t *a, uint64_t *b) const {
         uint64_t j = seg / segs_per_block, r = seg % segs_per_block;
-        uint64_t blk = (uint64_t)shard + j * nshards;
+        uint64_t blk = shard_block(j, shard, nshards);
         uint64_t bs = lo + blk * block;           // may exceed hi for trailing segments
         uint64_t s = bs + r * (uint64_t)SIEVE_SPAN;
         uint64_t e = s + SIEVE_SPAN;
@@ -136,7 +144,7 @@ template <typename T>
 __global__ void __launch_bounds__(SIEVE_THREADS)
 sieve_write_kernel(SegMap map, const uint32_t *__restrict__ bitmap, const uint64_t *__restrict__ seg_off,
                    T *__restrict__ out, uint64_t cap) {
-    constexpr int WPT = SIEVE_WORDS / SIEVE_THREADS;   // 4 words per thread
+    constexpr int WPT = SIEVE_WORDS / SIEVE_THREADS;   // 2 words per thread
     const uint64_t seg = blockIdx.x;
     uint64_t a, b;
     map.range(seg, &a, &b);

@@ -87,6 +87,8 @@ def test_gloo_gather_equals_single_process(world):
     assert all(a[1] == b[0] for a, b in zip(blocks_all, blocks_all[1:]))
     mine = {rank: blocks for rank, _, _, _, blocks in outs}
     assert mine[0][0][0] == LO and mine[1][0][0] == LO + BLOCK
+    # snake interleave: round 1 is dealt in reverse (block 2 -> rank 1, block 3 -> rank 0)
+    assert mine[1][1][0] == LO + 2 * BLOCK and mine[0][1][0] == LO + 3 * BLOCK
 
 
 def test_shard_blocks_default_block_sizes():
