@@ -189,7 +189,19 @@ typedef struct {
     wv_term  t[33];
 } wv_congruence;
 int wv_congruence_count(void);
-int wv_congruence_get(int id, wv_congruence *out);
+int wv_congruence_get(int id, wv_congruence *out);   /* WV_EINVAL if m > 33 or |a| >= 2^63 */
+
+/* Any congruence, including the generated many-sum ones (NEXT-2): coefficients and the
+ * left factor are sign + 128-bit magnitude (hi * 2^64 + lo).  seg = 1 means the kernels
+ * cut its work into sum-aligned chunks. */
+typedef struct {
+    char name[8];
+    uint64_t L_lo, L_hi;
+    uint32_t L_neg, e, m, min_p, excluded_p, seg;
+} wv_cong_header;
+typedef struct { uint64_t a_lo, a_hi; uint32_t neg, xn, xd, yn, yd; } wv_term128;
+int wv_congruence_header(int id, wv_cong_header *out);
+int wv_congruence_term(int id, uint32_t j, wv_term128 *out);
 
 /* Schedule override for tests and benchmarking (process-global, not
  * thread-safe): force congruence ids for W and V (-1 restores the default
@@ -197,7 +209,10 @@ int wv_congruence_get(int id, wv_congruence *out);
  * invalid forced choice for some p gives WV_EINVAL from the search. */
 int wv_set_schedule_override(int w_id, int v_id);
 /* Default schedule: W: p = 5 BB1, p = 7 VOR12, 11 <= p < 4096 BB1, p >= 4096 BB30;
- *                   V: p < 4096 EE3, p >= 4096 EE33.  Returns the id used. */
+ *                   V: p < 4096 EE3, p >= 4096 EE33;
+ * then, for large p, the generated many-sum congruences "BG_MID" (W, p >= 2^28),
+ * "BG_BIG" (W, p >= 2^34), "EG_MID" (V, p >= 2^26), "EG_BIG" (V, p >= 2^32) when the
+ * library was built with them (congruences_gen.inc).  Returns the id used. */
 int wv_schedule(uint64_t p, uint32_t test /* WV_MODE_W or WV_MODE_V */);
 
 /* Measurement hooks (process-wide, for bench.py / profiling).  When enabled,

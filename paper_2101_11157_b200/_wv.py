@@ -36,6 +36,17 @@ class _Term(ctypes.Structure):
                 ("yn", ctypes.c_uint32), ("yd", ctypes.c_uint32)]
 
 
+class _CongHdr(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 8), ("L_lo", ctypes.c_uint64), ("L_hi", ctypes.c_uint64),
+                ("L_neg", ctypes.c_uint32), ("e", ctypes.c_uint32), ("m", ctypes.c_uint32),
+                ("min_p", ctypes.c_uint32), ("excluded_p", ctypes.c_uint32), ("seg", ctypes.c_uint32)]
+
+
+class _Term128(ctypes.Structure):
+    _fields_ = [("a_lo", ctypes.c_uint64), ("a_hi", ctypes.c_uint64), ("neg", ctypes.c_uint32),
+                ("xn", ctypes.c_uint32), ("xd", ctypes.c_uint32), ("yn", ctypes.c_uint32), ("yd", ctypes.c_uint32)]
+
+
 class _Cong(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 8), ("L", ctypes.c_int64), ("e", ctypes.c_uint32),
                 ("m", ctypes.c_uint32), ("min_p", ctypes.c_uint32), ("excluded_p", ctypes.c_uint32),
@@ -66,6 +77,8 @@ SIGNATURES = {
     "wv_checksum_term": (_u64, [_u64, _u64, _u64]),
     "wv_congruence_count": (_i, []),
     "wv_congruence_get": (_i, [_i, _P(_Cong)]),
+    "wv_congruence_header": (_i, [_i, _P(_CongHdr)]),
+    "wv_congruence_term": (_i, [_i, _u32, _P(_Term128)]),
     "wv_set_schedule_override": (_i, [_i, _i]),
     "wv_schedule": (_i, [_u64, _u32]),
     "wv_stats_enable": (_i, [_i]),
@@ -290,14 +303,21 @@ def checksum_term(p, rw, rv):
 
 
 def congruences():
-    """The library's congruence table as a list of dicts."""
+    """The library's congruence table as a list of dicts (Python-int coefficients)."""
     L = lib()
     out = []
     for i in range(L.wv_congruence_count()):
-        c = _Cong()
-        _check(L.wv_congruence_get(i, ctypes.byref(c)))
-        out.append(dict(id=i, name=c.name.decode(), L=c.L, e=c.e, min_p=c.min_p, excluded_p=c.excluded_p,
-                        terms=[(c.t[j].a, c.t[j].xn, c.t[j].xd, c.t[j].yn, c.t[j].yd) for j in range(c.m)]))
+        h = _CongHdr()
+        _check(L.wv_congruence_header(i, ctypes.byref(h)))
+        lft = (h.L_hi << 64) | h.L_lo
+        terms = []
+        for j in range(h.m):
+            t = _Term128()
+            _check(L.wv_congruence_term(i, j, ctypes.byref(t)))
+            a = (t.a_hi << 64) | t.a_lo
+            terms.append((-a if t.neg else a, t.xn, t.xd, t.yn, t.yd))
+        out.append(dict(id=i, name=h.name.decode(), L=-lft if h.L_neg else lft, e=h.e, min_p=h.min_p,
+                        excluded_p=h.excluded_p, seg=h.seg, terms=terms))
     return out
 
 

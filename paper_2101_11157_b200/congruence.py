@@ -234,10 +234,12 @@ def best_move(c, D):
     return best
 
 
-def greedy_fast(c, rounds, D=8, verbose=False, stop_at=None):
+def greedy_fast(c, rounds, D=8, verbose=False, stop_at=None, on_round=None):
     """Section 2.2 heuristic with lambda = 1: apply the best single subdivision while it lowers the cost."""
     cur = c.normalize()
     for r in range(rounds):
+        if on_round is not None:
+            on_round(r, cur)
         mv = best_move(cur, D)
         if mv is None or mv[0] >= 0:
             break

@@ -25,11 +25,90 @@
 using namespace wv;
 
 // ------------------------------------------------------------------ constants
+// default schedule: the printed congruences, plus generated many-sum ones (if present) for large p;
+// finalised in sched_init() once the generated table is known
+static Sched g_sched = {{{0, 4096, 0, 0}, {0, 4096, 0, 0}}, {{C_BB1, C_BB30, 0, 0}, {C_EE3, C_EE33, 0, 0}}, {2, 2}, -1, -1};
+// printed congruences of the paper (int64 coefficients, <= 33 sums)
+struct SmallTerm { int64_t a; uint32_t xn, xd, yn, yd; };
+struct SmallCong { char name[8]; int64_t L; uint32_t e, m, min_p, excluded_p; SmallTerm t[33]; };
 #define WV_CONG(NAME, L, E, M, MINP, EXCL, ...) {NAME, (int64_t)(L), E, M, MINP, EXCL, __VA_ARGS__},
-static const Cong h_cong[NCONG] = {
+static const SmallCong h_small[] = {
 #include "congruences.inc"
 };
 #undef WV_CONG
+static const int NSMALL = sizeof h_small / sizeof h_small[0];
+
+// generated congruences (scripts/gen_congruences.py -> congruences_gen.inc): 128-bit coefficients
+struct GenCong { const char *name; uint32_t L_neg; uint64_t L_hi, L_lo; uint32_t e, m, min_p, excluded_p, seg; };
+struct GenTerm { uint32_t neg; uint64_t hi, lo; uint32_t xn, xd, yn, yd; };
+#include "congruences_gen.inc"
+
+// generated-congruence tiers (name, test, threshold): names from congruences_gen.inc
+struct GenTier { const char *name; int test; uint64_t th; };
+static const GenTier kGenTiers[] = {
+    {"BG_MID", 0, 1ull << 28}, {"BG_BIG", 0, 1ull << 34}, {"EG_MID", 1, 1ull << 26}, {"EG_BIG", 1, 1ull << 32},
+};
+
+// uniform host copy of every congruence: headers + one term array (uploaded per device)
+struct Table {
+    std::vector<Cong> hdr;
+    std::vector<Term> terms;
+    Table() {
+        for (int i = 0; i < NSMALL; i++) {
+            const SmallCong &s = h_small[i];
+            Cong c{};
+            memcpy(c.name, s.name, 8);
+            c.L_lo = (uint64_t)(s.L < 0 ? -s.L : s.L);
+            c.L_hi = 0;
+            c.L_neg = s.L < 0;
+            c.e = s.e; c.m = s.m; c.min_p = s.min_p; c.excluded_p = s.excluded_p;
+            c.seg = 0;
+            c.off = (uint32_t)terms.size();
+            for (uint32_t j = 0; j < s.m; j++) {
+                const SmallTerm &t = s.t[j];
+                terms.push_back(Term{(uint64_t)(t.a < 0 ? -t.a : t.a), 0, t.a < 0 ? 1u : 0u, t.xn, t.xd, t.yn, t.yd, 0});
+            }
+            hdr.push_back(c);
+        }
+        uint32_t k = 0;
+        for (int i = 0; i < NGEN; i++) {
+            const GenCong &g = kGenCong[i];
+            Cong c{};
+            strncpy(c.name, g.name, 7);
+            c.L_lo = g.L_lo; c.L_hi = g.L_hi; c.L_neg = g.L_neg;
+            c.e = g.e; c.m = g.m; c.min_p = g.min_p; c.excluded_p = g.excluded_p; c.seg = g.seg;
+            c.off = (uint32_t)terms.size();
+            for (uint32_t j = 0; j < g.m; j++, k++) {
+                const GenTerm &t = kGenTerms[k];
+                terms.push_back(Term{t.lo, t.hi, t.neg, t.xn, t.xd, t.yn, t.yd, 0});
+            }
+            hdr.push_back(c);
+        }
+    }
+};
+static void sched_init(const Table &t);
+static const Table &table() {
+    static Table t;
+    static bool once = false;
+    if (!once) {
+        once = true;
+        sched_init(t);
+    }
+    return t;
+}
+static void sched_init(const Table &t) {
+    for (const GenTier &g : kGenTiers) {
+        for (size_t i = NSMALL; i < t.hdr.size(); i++) {
+            if (strncmp(t.hdr[i].name, g.name, 7) != 0) continue;
+            int &n = g_sched.n[g.test];
+            if (n < 4) {
+                g_sched.th[g.test][n] = g.th;
+                g_sched.id[g.test][n] = (int)i;
+                n++;
+            }
+        }
+    }
+}
 
 // odd primes below 256: the bootstrap list that sieves [3, 65536)
 static const uint32_t h_boot[] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59, 61, 67,
@@ -41,7 +120,6 @@ static const uint64_t BASE0_HI = 65536;
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
 static std::atomic<uint64_t> g_launches{0};
-static Sched g_sched = {4096, C_BB1, C_BB30, C_EE3, C_EE33, -1, -1};
 
 // measurement hooks
 static std::atomic<int> g_stats_on{0};
@@ -142,7 +220,18 @@ static int ctx_get(DevCtx **out) {
         if (prop.major != 10)
             return set_err(WV_ECUDA, "libwv.so is built for sm_100a; device %d is sm_%d%d", dev, prop.major, prop.minor);
         c.sms = prop.multiProcessorCount;
-        CK(cudaMemcpyToSymbol(c_cong, h_cong, sizeof h_cong));
+        {
+            const Table &T = table();
+            if (T.hdr.size() > (size_t)NCONG_MAX) return set_err(WV_ECUDA, "too many congruences");
+            const int nc = (int)T.hdr.size();
+            CK(cudaMemcpyToSymbol(c_cong, T.hdr.data(), T.hdr.size() * sizeof(Cong)));
+            CK(cudaMemcpyToSymbol(c_ncong, &nc, sizeof nc));
+            Term *dt = nullptr;
+            CK(cudaMalloc(&dt, T.terms.size() * sizeof(Term)));
+            CK(cudaMemcpy(dt, T.terms.data(), T.terms.size() * sizeof(Term), cudaMemcpyHostToDevice));
+            const Term *dtc = dt;
+            CK(cudaMemcpyToSymbol(c_terms, &dtc, sizeof dtc));
+        }
         for (int v = 0; v < NVAR; v++) {
             if (kVariants[v].fn)
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[v], kVariants[v].fn, RES_THREADS, 0));
@@ -392,6 +481,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             CK(cudaMemsetAsync(misc + M_TERMS, 0, 24, st));
         }
         if (K > 0) {
+            (void)table();
             LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
                    nch, (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
                    (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr);
@@ -829,19 +919,50 @@ extern "C" int wv_shard_blocks(uint64_t lo, uint64_t hi, uint32_t shard, uint32_
 // ------------------------------------------------------------------ utilities
 extern "C" uint64_t wv_checksum_term(uint64_t p, uint64_t res_w, uint64_t res_v) { return checksum_term(p, res_w, res_v); }
 
-extern "C" int wv_congruence_count(void) { return NCONG; }
+extern "C" int wv_congruence_count(void) { return (int)table().hdr.size(); }
 
 extern "C" int wv_congruence_get(int id, wv_congruence *out) {
-    if (id < 0 || id >= NCONG || !out) return set_err(WV_EINVAL, "congruence id %d", id);
-    static_assert(sizeof(wv_congruence) == sizeof(Cong), "wv_congruence layout");
-    memcpy(out, &h_cong[id], sizeof(Cong));
+    const Table &T = table();
+    if (id < 0 || id >= (int)T.hdr.size() || !out) return set_err(WV_EINVAL, "congruence id %d", id);
+    const Cong &c = T.hdr[id];
+    if (c.m > 33 || c.L_hi || c.L_lo >> 63) return set_err(WV_EINVAL, "congruence %d does not fit wv_congruence", id);
+    memset(out, 0, sizeof *out);
+    memcpy(out->name, c.name, 8);
+    out->L = c.L_neg ? -(int64_t)c.L_lo : (int64_t)c.L_lo;
+    out->e = c.e; out->m = c.m; out->min_p = c.min_p; out->excluded_p = c.excluded_p;
+    for (uint32_t j = 0; j < c.m; j++) {
+        const Term &t = T.terms[c.off + j];
+        if (t.a_hi || t.a_lo >> 63) return set_err(WV_EINVAL, "coefficient too large");
+        out->t[j] = wv_term{t.neg ? -(int64_t)t.a_lo : (int64_t)t.a_lo, t.xn, t.xd, t.yn, t.yd};
+    }
+    return WV_OK;
+}
+
+extern "C" int wv_congruence_header(int id, wv_cong_header *out) {
+    const Table &T = table();
+    if (id < 0 || id >= (int)T.hdr.size() || !out) return set_err(WV_EINVAL, "congruence id %d", id);
+    const Cong &c = T.hdr[id];
+    memcpy(out->name, c.name, 8);
+    out->L_lo = c.L_lo; out->L_hi = c.L_hi; out->L_neg = c.L_neg;
+    out->e = c.e; out->m = c.m; out->min_p = c.min_p; out->excluded_p = c.excluded_p; out->seg = c.seg;
+    return WV_OK;
+}
+
+extern "C" int wv_congruence_term(int id, uint32_t j, wv_term128 *out) {
+    const Table &T = table();
+    if (id < 0 || id >= (int)T.hdr.size() || !out || j >= T.hdr[id].m) return set_err(WV_EINVAL, "term %d/%u", id, j);
+    const Term &t = T.terms[T.hdr[id].off + j];
+    out->a_lo = t.a_lo; out->a_hi = t.a_hi; out->neg = t.neg;
+    out->xn = t.xn; out->xd = t.xd; out->yn = t.yn; out->yd = t.yd;
     return WV_OK;
 }
 
 extern "C" int wv_set_schedule_override(int w_id, int v_id) {
-    if (w_id >= NCONG || v_id >= NCONG) return set_err(WV_EINVAL, "congruence id out of range");
-    if (w_id >= 0 && h_cong[w_id].e != 3) return set_err(WV_EINVAL, "%s is not a Bernoulli congruence", h_cong[w_id].name);
-    if (v_id >= 0 && h_cong[v_id].e != 2) return set_err(WV_EINVAL, "%s is not an Euler congruence", h_cong[v_id].name);
+    const Table &T = table();
+    const int n = (int)T.hdr.size();
+    if (w_id >= n || v_id >= n) return set_err(WV_EINVAL, "congruence id out of range");
+    if (w_id >= 0 && T.hdr[w_id].e != 3) return set_err(WV_EINVAL, "%s is not a Bernoulli congruence", T.hdr[w_id].name);
+    if (v_id >= 0 && T.hdr[v_id].e != 2) return set_err(WV_EINVAL, "%s is not an Euler congruence", T.hdr[v_id].name);
     g_sched.w_force = w_id < 0 ? -1 : w_id;
     g_sched.v_force = v_id < 0 ? -1 : v_id;
     return WV_OK;
@@ -849,6 +970,7 @@ extern "C" int wv_set_schedule_override(int w_id, int v_id) {
 
 extern "C" int wv_schedule(uint64_t p, uint32_t test) {
     if (test != WV_MODE_W && test != WV_MODE_V) return set_err(WV_EINVAL, "test must be W or V");
+    (void)table();
     return schedule(g_sched, p, test == WV_MODE_W ? 0 : 1);
 }
 

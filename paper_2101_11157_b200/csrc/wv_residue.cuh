@@ -23,19 +23,37 @@
 #pragma once
 #include <stdint.h>
 #include "wv_mont.cuh"
+#include "wv_scan.cuh"
 
 namespace wv {
 
-struct Term { int64_t a; uint32_t xn, xd, yn, yd; };
+// A congruence  L X == sum_j a_j S(x_j, y_j)  (mod p).  Coefficients are stored as
+// sign + 128-bit magnitude (generated congruences have ~80-bit integers); headers
+// live in constant memory, terms in a global array (lanes read different terms).
+struct Term { uint64_t a_lo, a_hi; uint32_t neg, xn, xd, yn, yd, pad; };       // 40 bytes
 struct Cong {
     char name[8];
-    int64_t L;
-    uint32_t e, m, min_p, excluded_p;
-    Term t[33];
+    uint64_t L_lo, L_hi;
+    uint32_t L_neg, e, m, min_p, excluded_p;
+    uint32_t seg;           // 1: sum-aligned chunking (many-sum congruences)
+    uint32_t off;           // index of term 0 in c_terms
+    uint32_t pad;
 };
 
-constexpr int NCONG = 14;
-__constant__ Cong c_cong[NCONG];
+constexpr int NCONG_MAX = 32;
+__constant__ Cong c_cong[NCONG_MAX];
+__constant__ int c_ncong;
+__constant__ const Term *c_terms;
+
+// (a_hi 2^64 + a_lo) * (-1)^neg  mod p, in [0, p)
+__device__ __forceinline__ uint64_t big_mod(uint64_t lo, uint64_t hi, uint32_t neg, uint64_t p) {
+    uint64_t r;
+    if (hi == 0) r = lo < p ? lo : lo % p;
+    else r = (uint64_t)((((unsigned __int128)hi << 64) | lo) % p);
+    return neg ? (r ? p - r : 0) : r;
+}
+__device__ __forceinline__ uint64_t coef_mod(const Term &t, uint64_t p) { return big_mod(t.a_lo, t.a_hi, t.neg, p); }
+__device__ __forceinline__ uint64_t left_mod(const Cong &c, uint64_t p) { return big_mod(c.L_lo, c.L_hi, c.L_neg, p); }
 
 struct Rec {                // one (prime, test) pair; 32 bytes
     uint64_t p;
@@ -46,9 +64,11 @@ struct Rec {                // one (prime, test) pair; 32 bytes
     uint32_t test;          // 0 = W (B_{p-3}), 1 = V (E_{p-3})
 };
 
-struct Sched {              // default schedule + overrides
-    uint64_t small;         // p < small uses the one-sum forms
-    int w_small, w_big, v_small, v_big;   // congruence ids
+struct Sched {              // tiered schedule + overrides
+    // test t (0 = W, 1 = V): use id[t][i] for the largest i with p >= th[t][i] (th[t][0] = 0)
+    uint64_t th[2][4];
+    int id[2][4];
+    int n[2];
     int w_force, v_force;   // -1 = none
 };
 
@@ -68,10 +88,13 @@ __host__ __device__ __forceinline__ int schedule(const Sched &s, uint64_t p, int
     if (test == 0) {
         if (s.w_force >= 0) return s.w_force;
         if (p == 7) return C_VOR12;
-        return p < s.small ? s.w_small : s.w_big;
+    } else if (s.v_force >= 0) {
+        return s.v_force;
     }
-    if (s.v_force >= 0) return s.v_force;
-    return p < s.small ? s.v_small : s.v_big;
+    int id = s.id[test][0];
+    for (int i = 1; i < s.n[test]; i++)
+        if (p >= s.th[test][i]) id = s.id[test][i];
+    return id;
 }
 
 // first and count of integers s with x p < s < y p  (x = xn/xd, y = yn/yd), exact.
@@ -111,7 +134,7 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         const uint32_t test = (mode == 3) ? (uint32_t)(k % ntests) : (mode == 1 ? 0u : 1u);
         const uint64_t p = primes[i];
         const int cid = schedule(sched, p, (int)test);
-        if (cid < 0 || cid >= NCONG || p < c_cong[cid].min_p || p == c_cong[cid].excluded_p ||
+        if (cid < 0 || cid >= c_ncong || p < c_cong[cid].min_p || p == c_cong[cid].excluded_p ||
             (test == 0) != (c_cong[cid].e == 3) || p < 5 || p >= (1ull << 62)) {
             atomicExch(err, 1);
             nchunks[k] = 0; recs[k].T = 0; recs[k].p = 0; continue;
@@ -120,13 +143,22 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         uint64_t T = 0;
         for (uint32_t j = 0; j < c.m; j++) {
             uint64_t f, cnt;
-            sum_bounds(p, c.t[j], &f, &cnt);
+            sum_bounds(p, c_terms[c.off + j], &f, &cnt);
             T += cnt;
         }
         uint64_t L = (T + 32ull * CAP_CHUNKS - 1) / (32ull * CAP_CHUNKS);
         if (L < LMIN) L = LMIN;
         if (L > 0x40000000ull) L = 0x40000000ull;
         uint64_t nc = (T + 32 * L - 1) / (32 * L);
+        if (c.seg) {                                   // sum-aligned chunks: ceil(n_j / CT) per sum
+            const uint64_t CT = 32 * L;
+            nc = 0;
+            for (uint32_t j = 0; j < c.m; j++) {
+                uint64_t f, cnt;
+                sum_bounds(p, c_terms[c.off + j], &f, &cnt);
+                nc += (cnt + CT - 1) / CT;
+            }
+        }
         if (gq && p < WIDTH32_MAX) {
             // lane mode: group g = 32 consecutive primes of this test, one per lane; Q slices,
             // Q fixed by the group's last prime so all 32 records agree (T grows with p)
@@ -135,10 +167,10 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
             const uint64_t pl = primes[il];
             const int cl = schedule(sched, pl, (int)test);
             uint64_t Tl = 0;
-            if (cl >= 0 && cl < NCONG)
+            if (cl >= 0 && cl < c_ncong)
                 for (uint32_t jj = 0; jj < c_cong[cl].m; jj++) {
                     uint64_t f, cnt;
-                    sum_bounds(pl, c_cong[cl].t[jj], &f, &cnt);
+                    sum_bounds(pl, c_terms[c_cong[cl].off + jj], &f, &cnt);
                     Tl += cnt;
                 }
             uint64_t Q = (Tl + LANE_SLICE - 1) / LANE_SLICE;
@@ -315,7 +347,7 @@ constexpr int RES_WARPS = RES_THREADS / 32;
 // stepping on dead state (ignored).  The FP64 engine range-reduces its u (and
 // d1) every rb terms, counted warp-uniformly.
 template <class M, class R, int E, int S, bool PAIRS>
-__device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Cong &cg, uint64_t p,
+__device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Term *terms, uint64_t p,
                                           const uint64_t *first, const uint64_t *cum, uint64_t t0, uint64_t t1,
                                           typename M::W &C0, typename M::W &C1) {
     using W = typename M::W;
@@ -392,7 +424,7 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Con
             if (nrun[i] == 0) {
                 W c0, c1;
                 run[i].result(mo, md, c0, c1);
-                c1 = mo.mul(c1, mo.mul((W)smod(cg.t[j[i]].a, p), mo.r2));   // fold a_j
+                c1 = mo.mul(c1, mo.mul((W)coef_mod(terms[j[i]], p), mo.r2));   // fold a_j
                 combine(mo, C0, C1, c0, c1);
                 if (t[i] < te[i]) {
                     j[i]++;
@@ -434,36 +466,77 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         const uint32_t m = cg.m;
         M mo;
         mo.init(r.p);
-        for (uint32_t j = lane; j < m; j += 32) {
-            uint64_t f, cnt;
-            sum_bounds(r.p, cg.t[j], &f, &cnt);
-            s_first[wid][j] = f;
-            s_cum[wid][j + 1] = cnt;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            uint64_t acc = 0;
-            s_cum[wid][0] = 0;
-            for (uint32_t j = 0; j < m; j++) { acc += s_cum[wid][j + 1]; s_cum[wid][j + 1] = acc; }
-        }
-        __syncwarp();
         const uint64_t CT = 32ull * r.L;
-        const uint64_t base = c * CT;
-        const uint64_t nck = (r.T - base) < CT ? (r.T - base) : CT;
-        const uint64_t per = (nck + 31) >> 5;
-        uint64_t t0 = base + lane * per;
-        uint64_t t1 = t0 + per;
-        const uint64_t tend = base + nck;
-        if (t1 > tend) t1 = tend;
+        const Term *tb = c_terms + cg.off;       // this record's terms
+        uint64_t sfirst[1], scum[2];
+        const uint64_t *first_p, *cum_p;
+        uint64_t t0, t1;
+        if (cg.seg) {
+            // sum-aligned chunk: locate (sum js, chunk cc) of local chunk c by a warp scan of
+            // ceil(n_j / CT) over the sums, 32 sums per round
+            uint64_t carry = 0, sf = 0, sn = 0, cc = 0;
+            uint32_t js = 0;
+            for (uint32_t base = 0; base < m; base += 32) {
+                const uint32_t jj = base + lane;
+                uint64_t f = 0, n = 0;
+                if (jj < m) sum_bounds(r.p, tb[jj], &f, &n);
+                const uint64_t ch = (n + CT - 1) / CT;
+                const uint64_t inc = warp_incl_scan(ch);
+                const uint32_t hit = __ballot_sync(0xffffffffu, carry + inc > c);
+                if (hit) {
+                    const int l0 = __ffs(hit) - 1;
+                    const uint64_t inc0 = __shfl_sync(0xffffffffu, inc, l0), ch0 = __shfl_sync(0xffffffffu, ch, l0);
+                    sf = __shfl_sync(0xffffffffu, f, l0);
+                    sn = __shfl_sync(0xffffffffu, n, l0);
+                    cc = c - (carry + inc0 - ch0);
+                    js = base + l0;
+                    break;
+                }
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            const uint64_t a0 = cc * CT, len = (sn - a0) < CT ? (sn - a0) : CT;
+            const uint64_t per = (len + 31) >> 5;
+            t0 = lane * per;
+            t1 = t0 + per < len ? t0 + per : len;
+            sfirst[0] = sf + a0;
+            scum[0] = 0;
+            scum[1] = len;
+            first_p = sfirst;
+            cum_p = scum;
+            tb += js;
+        } else {
+            for (uint32_t j = lane; j < m; j += 32) {
+                uint64_t f, cnt;
+                sum_bounds(r.p, tb[j], &f, &cnt);
+                s_first[wid][j] = f;
+                s_cum[wid][j + 1] = cnt;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                uint64_t acc = 0;
+                s_cum[wid][0] = 0;
+                for (uint32_t j = 0; j < m; j++) { acc += s_cum[wid][j + 1]; s_cum[wid][j + 1] = acc; }
+            }
+            __syncwarp();
+            const uint64_t base = c * CT;
+            const uint64_t nck = (r.T - base) < CT ? (r.T - base) : CT;
+            const uint64_t per = (nck + 31) >> 5;
+            t0 = base + lane * per;
+            t1 = t0 + per;
+            const uint64_t tend = base + nck;
+            if (t1 > tend) t1 = tend;
+            first_p = s_first[wid];
+            cum_p = s_cum[wid];
+        }
         W C0 = mo.r1, C1 = 0;
         ModD md;
         if (ENGINE == 1) {
             md.init(r.p);
-            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3, false>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
-            else lane_work<M, RunD<M, 2>, 2, S2, false>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3, false>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
+            else lane_work<M, RunD<M, 2>, 2, S2, false>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
         } else {
-            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3, PAIRS>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
-            else lane_work<M, Run<M, 2>, 2, S2, PAIRS>(mo, md, cg, r.p, s_first[wid], s_cum[wid], t0, t1, C0, C1);
+            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3, PAIRS>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
+            else lane_work<M, Run<M, 2>, 2, S2, PAIRS>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
         }
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -499,7 +572,7 @@ __device__ __forceinline__ void lane_slice_work(const M &mo, const ModD &md, con
         uint64_t s0 = 1;
         if (j < m) {
             uint64_t f, n;
-            sum_bounds(p, cg.t[j], &f, &n);
+            sum_bounds(p, c_terms[cg.off + j], &f, &n);
             const uint64_t a = n * q / Q, b = n * (q + 1) / Q;
             cnt = (uint32_t)(b - a);
             s0 = f + a;
@@ -531,7 +604,7 @@ __device__ __forceinline__ void lane_slice_work(const M &mo, const ModD &md, con
         if (cnt) {
             W c0, c1;
             run.result(mo, md, c0, c1);
-            c1 = mo.mul(c1, mo.mul((W)smod(cg.t[j].a, p), mo.r2));   // fold a_j
+            c1 = mo.mul(c1, mo.mul((W)coef_mod(c_terms[cg.off + j], p), mo.r2));   // fold a_j
             combine(mo, C0, C1, c0, c1);
         }
     }
@@ -593,7 +666,7 @@ __device__ __forceinline__ void finalize_one(const Rec &r, const uint64_t *start
         combine(mo, C0, C1, (W)v.x, (W)v.y);
     }
     const Cong &cg = c_cong[r.cid];
-    const W Lm = mo.mul((W)smod(cg.L, r.p), mo.r2);
+    const W Lm = mo.mul((W)left_mod(cg, r.p), mo.r2);
     const W den = mo.mul(C0, Lm);
     const W X = mo.mul(C1, mont_inv(mo, den));
     const uint64_t x = mo.canon(X);

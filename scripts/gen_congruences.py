@@ -30,7 +30,13 @@ def validate(c, pmax=2000):
 def main():
     name, rounds, D, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
     t0 = time.time()
-    c = greedy_fast(seed(name), rounds, D=D, verbose=True)
+
+    def dump(r, cur):          # checkpoint the history every 10 rounds (replayable)
+        if r % 10 == 0 and r:
+            json.dump(dict(seed=name, D=D, rounds=r, history=[(d, str(x), str(y)) for d, x, y in cur.history],
+                           r=float(1 / cur.cost()), m=cur.m()), open(out + ".partial", "w"))
+
+    c = greedy_fast(seed(name), rounds, D=D, verbose=True, on_round=dump)
     L, terms = c.integer_form()
     bad = validate(c)
     rec = dict(seed=name, rounds=rounds, D=D, cost=str(c.cost()), r=float(1 / c.cost()), m=c.m(), min_p=c.min_p,

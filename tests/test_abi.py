@@ -82,7 +82,7 @@ PAPER_COSTS = {
 
 
 def test_congruence_costs_match_paper(pkg):
-    table = pkg.congruences()
+    table = pkg.congruences()[: len(PAPER_COSTS)]
     assert [c["name"] for c in table] == list(PAPER_COSTS)
     for c in table:
         cost = sum(Fraction(yn, yd) - Fraction(xn, xd) for _, xn, xd, yn, yd in c["terms"])

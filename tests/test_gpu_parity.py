@@ -168,10 +168,10 @@ def test_every_congruence_on_gpu(wv):
     ps = sorted(set(rng.choice(small, 40, replace=False).tolist()) | {11, 13, 29989})
     big_w = [1025793739, 2139716869, 56604583391]       # Table 2
     big_v = [1062232319, 1836806681, 36652898767]       # Table 3 (sign-exact rows)
-    names = {c["name"]: c["id"] for c in wv.congruences()}
+    conf = {c["name"]: (c["id"], c["e"]) for c in wv.congruences()}
     try:
-        for name, cid in names.items():
-            e3 = name.startswith("BB") or name == "VOR12"
+        for name, (cid, e) in conf.items():
+            e3 = e == 3
             wv.set_schedule_override(cid if e3 else -1, -1 if e3 else cid)
             lst = ps + (big_w if e3 else big_v)
             rng.shuffle(lst)
