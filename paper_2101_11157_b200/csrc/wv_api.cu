@@ -46,7 +46,7 @@ struct GenTerm { uint32_t neg; uint64_t hi, lo; uint32_t xn, xd, yn, yd; };
 // generated-congruence tiers (name, test, threshold): names from congruences_gen.inc
 struct GenTier { const char *name; int test; uint64_t th; };
 static const GenTier kGenTiers[] = {
-    {"BG_MID", 0, 1ull << 28}, {"BG_BIG", 0, 1ull << 34}, {"EG_MID", 1, 1ull << 26}, {"EG_BIG", 1, 1ull << 32},
+    {"BG_MID", 0, 1ull << 29}, {"BG_BIG", 0, 1ull << 34}, {"EG_MID", 1, 1ull << 27}, {"EG_BIG", 1, 1ull << 32},
 };
 
 // uniform host copy of every congruence: headers + one term array (uploaded per device)

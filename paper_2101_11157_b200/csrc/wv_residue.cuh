@@ -99,11 +99,11 @@ __host__ __device__ __forceinline__ int schedule(const Sched &s, uint64_t p, int
 
 // first and count of integers s with x p < s < y p  (x = xn/xd, y = yn/yd), exact.
 __device__ __forceinline__ void sum_bounds(uint64_t p, const Term &t, uint64_t *first, uint64_t *count) {
-    if (p < (1ull << 32)) {                 // 32-bit division (den <= 2160, num < den)
+    if (p < (1ull << 32)) {                 // 32-bit divisions; num * rem may exceed 32 bits
         const uint32_t p32 = (uint32_t)p;
         const uint32_t qx = p32 / t.xd, rx = p32 % t.xd, qy = p32 / t.yd, ry = p32 % t.yd;
-        const uint64_t fl = (uint64_t)t.xn * qx + (t.xn * rx) / t.xd;
-        const uint64_t ce = (uint64_t)t.yn * qy + (t.yn * ry + t.yd - 1) / t.yd;
+        const uint64_t fl = (uint64_t)t.xn * qx + ((uint64_t)t.xn * rx) / t.xd;
+        const uint64_t ce = (uint64_t)t.yn * qy + ((uint64_t)t.yn * ry + t.yd - 1) / t.yd;
         const uint64_t f = fl + 1, l = ce - 1;
         *first = f;
         *count = l >= f ? l - f + 1 : 0;
