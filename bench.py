@@ -64,16 +64,21 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling around the timed region (B200_PROFILING.md clocks line).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    Started before the warm-up (nvidia-smi needs ~0.1-0.3 s to emit its first sample), stopped
+    after the timed region; samples whose timestamp falls inside the region are kept (if the
+    region is shorter than the sampling period, the sample closest to its midpoint)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpus):
         self.gpus = set(gpus)
         self.proc = None
         self.path = f"/tmp/wv_clocks_{os.getpid()}.csv"
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -83,38 +88,50 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def stop(self):
+        import datetime
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.f.close()
-        sm, mx, reasons, power = [], [], set(), []
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
                 continue
             try:
-                if int(parts[0]) not in self.gpus:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if int(parts[1]) not in self.gpus:
                     continue
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-                power.append(float(parts[3]))
+                rows.append((ts, float(parts[2]), float(parts[3]), float(parts[4]),
+                             [n for n, v in zip(names, parts[6:10]) if v.lower().startswith("active")]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
         os.unlink(self.path)
-        if not sm:
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "power_w_max": max(power) if power else None}
+        inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= self.t1]
+        note = "inside timed region"
+        if not inside:
+            mid = (self.t0 + self.t1) / 2 if self.t0 is not None else rows[-1][0]
+            inside = [min(rows, key=lambda r: abs(r[0] - mid))]
+            note = "closest sample to the timed region (region shorter than the 50 ms period)"
+        sm = sorted(r[1] for r in inside)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": sorted({x for r in inside for x in r[4]}), "samples": len(inside),
+                "power_w_max": max(r[3] for r in inside), "note": note}
 
 
 def _window(name):
@@ -215,18 +232,19 @@ def main():
             return gather(ds)
         return None
 
+    clocks = ClockSampler(range(world) if rank == 0 else [])
+    if rank == 0:
+        clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     wv.stats_reset()
     wv.stats_enable(True)
     launches0 = wv.launch_count()
-    clocks = ClockSampler(range(world) if rank == 0 else [])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    if rank == 0:
-        clocks.start()
+    clocks.mark_start()
     evs = []
     for _ in range(args.steps):
         flush.fill_(1)                                  # L2 flush between steps (outside the events)
@@ -236,6 +254,7 @@ def main():
         b.record(stream)
         evs.append((a, b))
     torch.cuda.synchronize()
+    clocks.mark_end()
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if rank == 0 else None
