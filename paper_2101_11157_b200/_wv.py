@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwv.so")
+LIB_PATH = os.environ.get("WV_LIB") or os.path.join(_HERE, "libwv.so")   # WV_LIB: A/B builds only
 
 MODE_W, MODE_V, MODE_BOTH = 1, 2, 3
 RES_NONE = (1 << 64) - 1

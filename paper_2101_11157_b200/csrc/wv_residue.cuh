@@ -208,6 +208,29 @@ __device__ __forceinline__ uint64_t find_rec(const uint64_t *__restrict__ start,
     return lo;
 }
 
+// Same result, warp-cooperative (all 32 lanes, g warp-uniform): a 32-ary search, each round
+// probing 31 cut points at once -- log32 rounds of loads instead of log2 dependent ones.
+__device__ __forceinline__ uint64_t find_rec_warp(const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
+                                                  uint64_t g) {
+    const int lane = threadIdx.x & 31;
+    uint64_t lo = klo, hi = khi;          // invariant: start[lo] <= g < start[hi] (start[khi] = end)
+    while (hi - lo > 32) {
+        const uint64_t step = (hi - lo + 31) / 32;
+        const uint64_t idx = lo + (uint64_t)lane * step;             // lane 0 probes lo itself
+        const bool ok = idx < hi && start[idx] <= g;
+        const uint32_t m = __ballot_sync(0xffffffffu, ok);           // prefix of lanes (start ascending)
+        const int last = 31 - __clz(m);
+        const uint64_t nlo = lo + (uint64_t)last * step;
+        const uint64_t nhi = nlo + step < hi ? nlo + step : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    const uint64_t idx = lo + lane;
+    const bool ok = idx < hi && start[idx] <= g;
+    const uint32_t m = __ballot_sync(0xffffffffu, ok);
+    return lo + (31 - __clz(m));
+}
+
 // ---------------------------------------------------------------- term runs
 // A "run" is the state of consecutive terms s, s+1, ... of one sum: u = s^E,
 // its forward differences, and the pair (a0, a1) of prod (z + u).  Two
@@ -347,7 +370,7 @@ constexpr int RES_WARPS = RES_THREADS / 32;
 // stepping on dead state (ignored).  The FP64 engine range-reduces its u (and
 // d1) every rb terms, counted warp-uniformly.
 template <class M, class R, int E, int S, bool PAIRS>
-__device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Term *terms, uint64_t p,
+__device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const uint64_t *coefm, uint64_t p,
                                           const uint64_t *first, const uint64_t *cum, uint64_t t0, uint64_t t1,
                                           typename M::W &C0, typename M::W &C1) {
     using W = typename M::W;
@@ -379,6 +402,8 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Ter
             if (nrun[i] && nrun[i] < mn) mn = nrun[i];
         const uint32_t k = __reduce_min_sync(0xffffffffu, mn);
         if (k == 0xffffffffu) break;
+        // (batching run switches behind a window of masked steps was measured slower on C2:
+        //  23.4 ms unbatched vs 24.7 / 25.7 / 27.2 ms with 16 / 32 / 64-step windows)
         uint32_t left = k;
         while (left) {
             const uint32_t kk = left < rb - since ? left : rb - since;
@@ -424,7 +449,7 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const Ter
             if (nrun[i] == 0) {
                 W c0, c1;
                 run[i].result(mo, md, c0, c1);
-                c1 = mo.mul(c1, mo.mul((W)coef_mod(terms[j[i]], p), mo.r2));   // fold a_j
+                c1 = mo.mul(c1, (W)coefm[j[i]]);                               // fold a_j (Montgomery form)
                 combine(mo, C0, C1, c0, c1);
                 if (t[i] < te[i]) {
                     j[i]++;
@@ -453,6 +478,7 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
     using W = typename M::W;
     __shared__ uint64_t s_first[RES_WARPS][34];
     __shared__ uint64_t s_cum[RES_WARPS][35];
+    __shared__ uint64_t s_coef[RES_WARPS][34];       // a_j mod p, Montgomery form
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (;;) {
         unsigned long long gi = 0;
@@ -460,7 +486,7 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         gi = __shfl_sync(0xffffffffu, gi, 0);
         const uint64_t g = g_lo + gi;
         if (g >= g_hi) break;
-        const uint64_t k = find_rec(start, klo, khi, g);
+        const uint64_t k = find_rec_warp(start, klo, khi, g);
         const Rec r = recs[k];
         if (!((class_mask >> prime_class(r.p)) & 1)) continue;   // another class's launch does it
         const uint64_t c = g - start[k];
@@ -470,8 +496,6 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         mo.init(r.p);
         const uint64_t CT = 32ull * r.L;
         const Term *tb = c_terms + cg.off;       // this record's terms
-        uint64_t sfirst[1], scum[2];
-        const uint64_t *first_p, *cum_p;
         uint64_t t0, t1;
         if (cg.seg) {
             // sum-aligned chunk: locate (sum js, chunk cc) of local chunk c by a warp scan of
@@ -500,18 +524,20 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
             const uint64_t per = (len + 31) >> 5;
             t0 = lane * per;
             t1 = t0 + per < len ? t0 + per : len;
-            sfirst[0] = sf + a0;
-            scum[0] = 0;
-            scum[1] = len;
-            first_p = sfirst;
-            cum_p = scum;
-            tb += js;
+            if (lane == 0) {                           // a one-sum table for lane_work
+                s_first[wid][0] = sf + a0;
+                s_cum[wid][0] = 0;
+                s_cum[wid][1] = len;
+                s_coef[wid][0] = (uint64_t)mo.mul((W)coef_mod(tb[js], r.p), mo.r2);
+            }
+            __syncwarp();
         } else {
             for (uint32_t j = lane; j < m; j += 32) {
                 uint64_t f, cnt;
                 sum_bounds(r.p, tb[j], &f, &cnt);
                 s_first[wid][j] = f;
                 s_cum[wid][j + 1] = cnt;
+                s_coef[wid][j] = (uint64_t)mo.mul((W)coef_mod(tb[j], r.p), mo.r2);
             }
             __syncwarp();
             if (lane == 0) {
@@ -527,18 +553,17 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
             t1 = t0 + per;
             const uint64_t tend = base + nck;
             if (t1 > tend) t1 = tend;
-            first_p = s_first[wid];
-            cum_p = s_cum[wid];
         }
+        const uint64_t *first_p = s_first[wid], *cum_p = s_cum[wid], *coef_p = s_coef[wid];
         W C0 = mo.r1, C1 = 0;
         ModD md;
         if (ENGINE == 1) {
             md.init(r.p);
-            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3, false>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
-            else lane_work<M, RunD<M, 2>, 2, S2, false>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
+            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3, false>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
+            else lane_work<M, RunD<M, 2>, 2, S2, false>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
         } else {
-            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3, PAIRS>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
-            else lane_work<M, Run<M, 2>, 2, S2, PAIRS>(mo, md, tb, r.p, first_p, cum_p, t0, t1, C0, C1);
+            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3, PAIRS>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
+            else lane_work<M, Run<M, 2>, 2, S2, PAIRS>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
         }
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {

@@ -10,7 +10,7 @@ for name in names:
     w = CONFIGS.get(name) or SUBWINDOWS[name]
     ds = wv.DeviceSearch(w.lo, w.hi, w.mode)
     ds.run()
-    reps = 3 if name in ("c1", "c2") else 1
+    reps = int(os.environ.get("REPS", 3 if name in ("c1", "c2") else 1))
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     s.record()
