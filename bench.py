@@ -214,17 +214,9 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def gather(ds):
-        """NCCL all_gather of per-rank (n_primes, n_hits, checksum) and the hit lists."""
-        meta = torch.tensor([ds.n_primes, ds.n_hits, 0], dtype=torch.int64, device=dev)
-        meta[2:3].copy_(ds.checksum)
-        allm = [torch.empty_like(meta) for _ in range(world)]
-        dist.all_gather(allm, meta)
-        mh = max(int(m[1]) for m in allm)
-        hits = torch.zeros(2 * max(mh, 1), dtype=torch.int64, device=dev)
-        hits[: 2 * ds.n_hits].copy_(ds.hits[: 2 * ds.n_hits])
-        allh = [torch.empty_like(hits) for _ in range(world)]
-        dist.all_gather(allh, hits)
-        return allm, allh
+        """Per-rank hits/checksum -> all ranks (dist.gather_results over NCCL; gloo-tested on CPU)."""
+        from paper_2101_11157_b200.dist import gather_results
+        return gather_results(ds.hits_np(), None, ds.checksum_int(), device=dev)
 
     def step():
         ds.run(stream)

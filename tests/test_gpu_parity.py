@@ -352,3 +352,20 @@ def test_c3_wolstenholme_near_misses_table2(wv):
     exp = n / 2000
     chi2 = float((((hw.astype(np.float64) - exp) ** 2) / exp).sum())
     assert 1700 < chi2 < 2300            # 1999 degrees of freedom
+
+
+def test_bench_contract_line():
+    """bench.py (the driver's contract) runs on the GPU and prints one well-formed JSON line."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--ref-sample", "64"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in line, k
+    assert line["value"] > 1e5 and line["config"]["primes"] == 216814
+    assert 0 < line["roofline"]["frac"] <= 1.5 and line["gpu_launches"] > 0
+    assert line["e2e"]["d2h_bytes_per_step"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
