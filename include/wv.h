@@ -210,7 +210,8 @@ int wv_congruence_term(int id, uint32_t j, wv_term128 *out);
 int wv_set_schedule_override(int w_id, int v_id);
 /* Default schedule: W: p = 5 BB1, p = 7 VOR12, 11 <= p < 4096 BB1, p >= 4096 BB30;
  *                   V: p < 4096 EE3, p >= 4096 EE33;
- * then, for large p, the generated many-sum congruences "BG_MID" (W, p >= 2^29),
+ * then the generated congruences "BG_SML" / "EG_SML" (greedy continuations of BB30 / EE33,
+ * p >= 2^17), and for large p the many-sum "BG_MID" (W, p >= 2^29),
  * "BG_BIG" (W, p >= 2^34), "EG_MID" (V, p >= 2^27), "EG_BIG" (V, p >= 2^32) when the
  * library was built with them (congruences_gen.inc).  Returns the id used. */
 int wv_schedule(uint64_t p, uint32_t test /* WV_MODE_W or WV_MODE_V */);

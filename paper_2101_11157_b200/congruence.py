@@ -177,6 +177,13 @@ def seed(name):
         return Congruence.from_terms("E", -4, [(1, Fr(0), Fr(1, 4))], min_p=7)
     if name == "EMac2":         # eqnEMac2 at k = 1
         return Congruence.from_terms("E", -40, [(1, Fr(0), Fr(1, 12)), (-1, Fr(5, 12), HALF)], min_p=7)
+    if name.startswith("table:"):   # a congruence of the library's table (e.g. "table:BB30", eqnBB30)
+        from . import _wv
+        for c in _wv.congruences():
+            if c["name"] == name[6:]:
+                return Congruence.from_terms("B" if c["e"] == 3 else "E", c["L"],
+                                             [(a, Fr(xn, xd), Fr(yn, yd)) for a, xn, xd, yn, yd in c["terms"]],
+                                             min_p=max(11, c["min_p"]))
     raise KeyError(name)
 
 

@@ -27,7 +27,8 @@ using namespace wv;
 // ------------------------------------------------------------------ constants
 // default schedule: the printed congruences, plus generated many-sum ones (if present) for large p;
 // finalised in sched_init() once the generated table is known
-static Sched g_sched = {{{0, 4096, 0, 0}, {0, 4096, 0, 0}}, {{C_BB1, C_BB30, 0, 0}, {C_EE3, C_EE33, 0, 0}}, {2, 2}, -1, -1};
+static Sched g_sched = {{{0, 4096, 0, 0, 0, 0}, {0, 4096, 0, 0, 0, 0}},
+                        {{C_BB1, C_BB30, 0, 0, 0, 0}, {C_EE3, C_EE33, 0, 0, 0, 0}}, {2, 2}, -1, -1};
 // printed congruences of the paper (int64 coefficients, <= 33 sums)
 struct SmallTerm { int64_t a; uint32_t xn, xd, yn, yd; };
 struct SmallCong { char name[8]; int64_t L; uint32_t e, m, min_p, excluded_p; SmallTerm t[33]; };
@@ -45,8 +46,9 @@ struct GenTerm { uint32_t neg; uint64_t hi, lo; uint32_t xn, xd, yn, yd; };
 
 // generated-congruence tiers (name, test, threshold): names from congruences_gen.inc
 struct GenTier { const char *name; int test; uint64_t th; };
-static const GenTier kGenTiers[] = {
-    {"BG_MID", 0, 1ull << 29}, {"BG_BIG", 0, 1ull << 34}, {"EG_MID", 1, 1ull << 27}, {"EG_BIG", 1, 1ull << 32},
+static GenTier kGenTiers[] = {
+    {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 1ull << 29}, {"BG_BIG", 0, 1ull << 34},
+    {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 27}, {"EG_BIG", 1, 1ull << 32},
 };
 
 // uniform host copy of every congruence: headers + one term array (uploaded per device)
@@ -97,11 +99,18 @@ static const Table &table() {
     return t;
 }
 static void sched_init(const Table &t) {
+    // benchmarking knob: WV_SML_TH_W / WV_SML_TH_V override the small-tier thresholds (0 disables)
+    const char *ew = getenv("WV_SML_TH_W"), *ev = getenv("WV_SML_TH_V");
+    for (GenTier &g : kGenTiers) {
+        if (!strcmp(g.name, "BG_SML") && ew) g.th = strtoull(ew, nullptr, 0);
+        if (!strcmp(g.name, "EG_SML") && ev) g.th = strtoull(ev, nullptr, 0);
+    }
     for (const GenTier &g : kGenTiers) {
+        if (g.th == 0) continue;
         for (size_t i = NSMALL; i < t.hdr.size(); i++) {
             if (strncmp(t.hdr[i].name, g.name, 7) != 0) continue;
             int &n = g_sched.n[g.test];
-            if (n < 4) {
+            if (n < 6) {
                 g_sched.th[g.test][n] = g.th;
                 g_sched.id[g.test][n] = (int)i;
                 n++;

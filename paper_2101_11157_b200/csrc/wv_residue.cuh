@@ -66,13 +66,14 @@ struct Rec {                // one (prime, test) pair; 32 bytes
 
 struct Sched {              // tiered schedule + overrides
     // test t (0 = W, 1 = V): use id[t][i] for the largest i with p >= th[t][i] (th[t][0] = 0)
-    uint64_t th[2][4];
-    int id[2][4];
+    uint64_t th[2][6];
+    int id[2][6];
     int n[2];
     int w_force, v_force;   // -1 = none
 };
 
 constexpr uint32_t CAP_CHUNKS = 1024;   // target max chunks per record
+constexpr uint32_t MAX_CONTIG_M = 96;   // contiguous (non-seg) chunking handles congruences up to 96 sums
 constexpr uint32_t LMIN = 4096;         // min terms per lane in a full chunk
 constexpr uint64_t LANE_SLICE = 8192;   // lane mode: target terms per lane per slice
 constexpr uint64_t LANE_QMAX = 128;     // lane mode: max slices per record
@@ -300,6 +301,12 @@ struct Run {
     }
     __device__ __forceinline__ void reduce(const ModD &) {}
     __device__ __forceinline__ void result(const M &, const ModD &, W &c0, W &c1) const { c0 = a0; c1 = a1; }
+    // sum-start state (u, d1, d2) to / from shared memory, and a1 <- a1 * ratio (Montgomery form)
+    __device__ __forceinline__ void save_start(uint64_t *st) const { st[0] = u; st[1] = d1; st[2] = d2; }
+    __device__ __forceinline__ void load_start(const uint64_t *st) { u = (W)st[0]; d1 = (W)st[1]; d2 = (W)st[2]; }
+    __device__ __forceinline__ void scale1(const M &mo, const ModD &, uint64_t ratio_m, uint64_t) {
+        a1 = mo.mul(a1, (W)ratio_m);
+    }
 };
 
 template <class M, int E>
@@ -347,6 +354,19 @@ struct RunD {
         c0 = mo.mul((W)md.canon(a0), mo.r2);     // into the combine domain (Montgomery form)
         c1 = mo.mul((W)md.canon(a1), mo.r2);
     }
+    __device__ __forceinline__ void save_start(uint64_t *st) const {
+        st[0] = (uint64_t)__double_as_longlong(u);
+        st[1] = (uint64_t)__double_as_longlong(d1);
+        st[2] = (uint64_t)__double_as_longlong(d2);
+    }
+    __device__ __forceinline__ void load_start(const uint64_t *st) {
+        u = __longlong_as_double((long long)st[0]);
+        d1 = __longlong_as_double((long long)st[1]);
+        d2 = __longlong_as_double((long long)st[2]);
+    }
+    __device__ __forceinline__ void scale1(const M &, const ModD &md, uint64_t, uint64_t ratio_canon) {
+        a1 = md.mul(a1, (double)ratio_canon);   // |a1| <= 2p, ratio < p: |result| <= p
+    }
 };
 
 template <class M>
@@ -369,11 +389,58 @@ constexpr int RES_WARPS = RES_THREADS / 32;
 // re-seed u and its differences) runs where a run ended.  Finished streams keep
 // stepping on dead state (ignored).  The FP64 engine range-reduces its u (and
 // d1) every rb terms, counted warp-uniformly.
-template <class M, class R, int E, int S, bool PAIRS>
-__device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const uint64_t *coefm, uint64_t p,
-                                          const uint64_t *first, const uint64_t *cum, uint64_t t0, uint64_t t1,
-                                          typename M::W &C0, typename M::W &C1) {
+// Per-warp item tables in shared memory (contiguous chunking, up to MAX_CONTIG_M sums).
+struct WarpTab {
+    uint64_t first[MAX_CONTIG_M];       // first s of each sum
+    uint64_t cum[MAX_CONTIG_M + 1];     // prefix counts (flattened term space)
+    uint64_t coef[MAX_CONTIG_M];        // a_j mod p, Montgomery form
+    uint64_t st[MAX_CONTIG_M][3];       // run state (u, d1, d2) at s = first_j
+    uint64_t ratio[MAX_CONTIG_M];       // a_j / a_{j+1}: Montgomery form (IMAD) or canonical (FP64)
+    uint32_t cont;                      // 1: every a_j is a unit mod p -> continuous runs across sums
+};
+
+// Fill st[] and ratio[] (warp-cooperative) for the continuous switch: a stream that leaves sum j
+// at its end enters sum j+1 at its start, so it loads that sum's start state and rescales
+// a1 by a_j / a_{j+1}: the running pair then represents sum_j a_j S_j / a_{j+1} without a merge.
+template <class M, class R>
+__device__ __forceinline__ void prepare_switch(const M &mo, const ModD &md, WarpTab &tb, uint32_t m) {
     using W = typename M::W;
+    const int lane = threadIdx.x & 31;
+    bool unit = true;
+    for (uint32_t j = lane; j < m; j += 32) {
+        R tmp;
+        tmp.setup(mo, md, tb.first[j]);
+        tmp.save_start(tb.st[j]);
+        unit = unit && mo.canon((W)tb.coef[j]) != 0;
+    }
+    const bool all = __all_sync(0xffffffffu, unit);
+    if (lane == 0) tb.cont = all ? 1u : 0u;
+    if (all) {
+        W inv[3];
+        uint32_t k = 0;
+        for (uint32_t j = lane; j < m; j += 32, k++) inv[k] = mont_inv(mo, (W)tb.coef[j]);
+        __syncwarp();
+        k = 0;
+        for (uint32_t j = lane; j < m; j += 32, k++) tb.ratio[j] = inv[k];     // stash 1/a_j
+        __syncwarp();
+        W rr[3];
+        k = 0;
+        for (uint32_t j = lane; j < m; j += 32, k++)
+            rr[k] = (j + 1 < m) ? mo.mul((W)tb.coef[j], (W)tb.ratio[j + 1]) : (W)0;
+        __syncwarp();
+        k = 0;
+        for (uint32_t j = lane; j < m; j += 32, k++)
+            tb.ratio[j] = R::kFP ? mo.canon(rr[k]) : (uint64_t)rr[k];
+    }
+    __syncwarp();
+}
+
+template <class M, class R, int E, int S, bool PAIRS>
+__device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const WarpTab &tab, uint64_t p,
+                                          uint64_t t0, uint64_t t1, typename M::W &C0, typename M::W &C1) {
+    using W = typename M::W;
+    const uint64_t *coefm = tab.coef, *first = tab.first, *cum = tab.cum;
+    const bool cont = tab.cont != 0;
     R run[S];
     uint32_t j[S], nrun[S];
     uint64_t t[S], te[S];
@@ -447,15 +514,25 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const uin
             nrun[i] -= k;
             t[i] += k;
             if (nrun[i] == 0) {
-                W c0, c1;
-                run[i].result(mo, md, c0, c1);
-                c1 = mo.mul(c1, (W)coefm[j[i]]);                               // fold a_j (Montgomery form)
-                combine(mo, C0, C1, c0, c1);
-                if (t[i] < te[i]) {
-                    j[i]++;
-                    while (cum[j[i] + 1] <= t[i]) j[i]++;
+                if (cont && t[i] < te[i]) {
+                    // continuous switch: enter the next non-empty sum at its start
+                    do {
+                        run[i].scale1(mo, md, tab.ratio[j[i]], tab.ratio[j[i]]);
+                        j[i]++;
+                    } while (cum[j[i] + 1] <= t[i]);
+                    run[i].load_start(tab.st[j[i]]);
                     nrun[i] = (uint32_t)((te[i] < cum[j[i] + 1] ? te[i] : cum[j[i] + 1]) - t[i]);
-                    run[i].setup(mo, md, first[j[i]] + (t[i] - cum[j[i]]));
+                } else {
+                    W c0, c1;
+                    run[i].result(mo, md, c0, c1);
+                    c1 = mo.mul(c1, (W)coefm[j[i]]);                               // fold a_j (Montgomery form)
+                    combine(mo, C0, C1, c0, c1);
+                    if (t[i] < te[i]) {
+                        j[i]++;
+                        while (cum[j[i] + 1] <= t[i]) j[i]++;
+                        nrun[i] = (uint32_t)((te[i] < cum[j[i] + 1] ? te[i] : cum[j[i] + 1]) - t[i]);
+                        run[i].setup(mo, md, first[j[i]] + (t[i] - cum[j[i]]));
+                    }
                 }
             }
         }
@@ -476,9 +553,7 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
                unsigned long long *__restrict__ counter, uint32_t class_mask) {
     using W = typename M::W;
-    __shared__ uint64_t s_first[RES_WARPS][34];
-    __shared__ uint64_t s_cum[RES_WARPS][35];
-    __shared__ uint64_t s_coef[RES_WARPS][34];       // a_j mod p, Montgomery form
+    __shared__ WarpTab s_tab[RES_WARPS];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (;;) {
         unsigned long long gi = 0;
@@ -525,25 +600,32 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
             t0 = lane * per;
             t1 = t0 + per < len ? t0 + per : len;
             if (lane == 0) {                           // a one-sum table for lane_work
-                s_first[wid][0] = sf + a0;
-                s_cum[wid][0] = 0;
-                s_cum[wid][1] = len;
-                s_coef[wid][0] = (uint64_t)mo.mul((W)coef_mod(tb[js], r.p), mo.r2);
+                s_tab[wid].first[0] = sf + a0;
+                s_tab[wid].cum[0] = 0;
+                s_tab[wid].cum[1] = len;
+                s_tab[wid].coef[0] = (uint64_t)mo.mul((W)coef_mod(tb[js], r.p), mo.r2);
+                s_tab[wid].cont = 0;                   // one run per stream: nothing to switch
             }
             __syncwarp();
         } else {
             for (uint32_t j = lane; j < m; j += 32) {
                 uint64_t f, cnt;
                 sum_bounds(r.p, tb[j], &f, &cnt);
-                s_first[wid][j] = f;
-                s_cum[wid][j + 1] = cnt;
-                s_coef[wid][j] = (uint64_t)mo.mul((W)coef_mod(tb[j], r.p), mo.r2);
+                s_tab[wid].first[j] = f;
+                s_tab[wid].cum[j + 1] = cnt;
+                s_tab[wid].coef[j] = (uint64_t)mo.mul((W)coef_mod(tb[j], r.p), mo.r2);
             }
             __syncwarp();
-            if (lane == 0) {
-                uint64_t acc = 0;
-                s_cum[wid][0] = 0;
-                for (uint32_t j = 0; j < m; j++) { acc += s_cum[wid][j + 1]; s_cum[wid][j + 1] = acc; }
+            {                                          // warp-parallel prefix sums of the counts
+                uint64_t carry = 0;
+                for (uint32_t base = 0; base < m; base += 32) {
+                    const uint32_t j = base + lane;
+                    const uint64_t v = j < m ? s_tab[wid].cum[j + 1] : 0;
+                    const uint64_t inc = warp_incl_scan(v) + carry;
+                    if (j < m) s_tab[wid].cum[j + 1] = inc;
+                    carry = __shfl_sync(0xffffffffu, inc, 31);
+                }
+                if (lane == 0) s_tab[wid].cum[0] = 0;
             }
             __syncwarp();
             const uint64_t base = c * CT;
@@ -554,16 +636,31 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
             const uint64_t tend = base + nck;
             if (t1 > tend) t1 = tend;
         }
-        const uint64_t *first_p = s_first[wid], *cum_p = s_cum[wid], *coef_p = s_coef[wid];
         W C0 = mo.r1, C1 = 0;
         ModD md;
+        WarpTab &tab = s_tab[wid];
+        const bool prep = !cg.seg && m > 1;
+        if (!prep && !cg.seg) {
+            if (lane == 0) tab.cont = 0;
+            __syncwarp();
+        }
         if (ENGINE == 1) {
             md.init(r.p);
-            if (cg.e == 3) lane_work<M, RunD<M, 3>, 3, S3, false>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
-            else lane_work<M, RunD<M, 2>, 2, S2, false>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
+            if (cg.e == 3) {
+                if (prep) prepare_switch<M, RunD<M, 3>>(mo, md, tab, m);
+                lane_work<M, RunD<M, 3>, 3, S3, false>(mo, md, tab, r.p, t0, t1, C0, C1);
+            } else {
+                if (prep) prepare_switch<M, RunD<M, 2>>(mo, md, tab, m);
+                lane_work<M, RunD<M, 2>, 2, S2, false>(mo, md, tab, r.p, t0, t1, C0, C1);
+            }
         } else {
-            if (cg.e == 3) lane_work<M, Run<M, 3>, 3, S3, PAIRS>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
-            else lane_work<M, Run<M, 2>, 2, S2, PAIRS>(mo, md, coef_p, r.p, first_p, cum_p, t0, t1, C0, C1);
+            if (cg.e == 3) {
+                if (prep) prepare_switch<M, Run<M, 3>>(mo, md, tab, m);
+                lane_work<M, Run<M, 3>, 3, S3, PAIRS>(mo, md, tab, r.p, t0, t1, C0, C1);
+            } else {
+                if (prep) prepare_switch<M, Run<M, 2>>(mo, md, tab, m);
+                lane_work<M, Run<M, 2>, 2, S2, PAIRS>(mo, md, tab, r.p, t0, t1, C0, C1);
+            }
         }
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {

@@ -59,9 +59,10 @@ def test_host_utilities(pkg):
     names = {c["id"]: c["name"] for c in pkg.congruences()}
     assert names[pkg.schedule(5, pkg.MODE_W)] == "BB1"
     assert names[pkg.schedule(7, pkg.MODE_W)] == "VOR12"
-    assert names[pkg.schedule(10 ** 6, pkg.MODE_W)] == "BB30"
+    assert names[pkg.schedule(10 ** 5, pkg.MODE_W)] == "BB30"
     assert names[pkg.schedule(5, pkg.MODE_V)] == "EE3"
-    assert names[pkg.schedule(10 ** 6, pkg.MODE_V)] == "EE33"
+    assert names[pkg.schedule(10 ** 5, pkg.MODE_V)] == "EE33"
+    assert names[pkg.schedule(10 ** 6, pkg.MODE_W)] == "BG_SML" and names[pkg.schedule(10 ** 6, pkg.MODE_V)] == "EG_SML"
     # generated many-sum congruences (NEXT-2) for large p
     assert names[pkg.schedule(10 ** 9, pkg.MODE_W)] == "BG_MID" and names[pkg.schedule(10 ** 9, pkg.MODE_V)] == "EG_MID"
     assert names[pkg.schedule(5 * 10 ** 10, pkg.MODE_W)] == "BG_BIG"
