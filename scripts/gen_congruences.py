@@ -29,6 +29,7 @@ def validate(c, pmax=2000):
 
 def main():
     name, rounds, D, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+    resume = sys.argv[5] if len(sys.argv) > 5 else None     # history JSON to continue from
     t0 = time.time()
 
     def dump(r, cur):          # checkpoint the history every 10 rounds (replayable)
@@ -36,7 +37,12 @@ def main():
             json.dump(dict(seed=name, D=D, rounds=r, history=[(d, str(x), str(y)) for d, x, y in cur.history],
                            r=float(1 / cur.cost()), m=cur.m()), open(out + ".partial", "w"))
 
-    c = greedy_fast(seed(name), rounds, D=D, verbose=True, on_round=dump)
+    start = seed(name)
+    if resume:
+        from fractions import Fraction as Fr
+        from paper_2101_11157_b200.congruence import replay
+        start = replay(start, [(d, Fr(x), Fr(y)) for d, x, y in json.load(open(resume))["history"]])
+    c = greedy_fast(start, rounds, D=D, verbose=True, on_round=dump)
     L, terms = c.integer_form()
     bad = validate(c)
     rec = dict(seed=name, rounds=rounds, D=D, cost=str(c.cost()), r=float(1 / c.cost()), m=c.m(), min_p=c.min_p,
