@@ -40,6 +40,8 @@ UNIT = "primes/s"
 
 # Modular multiplications per term: c1 <- c1 u + c0, c0 <- c0 u
 MULMODS_PER_TERM = 2
+# SURVEY.md 8(d) per-unit figure: algorithmic terms per prime (BB30: 227/6480 p, EE33: 27/512 p)
+TERMS_PER_P = {1: 227 / 6480, 2: 27 / 512}
 # Roofline per prime class: (pipe, lanes/clk/SM, pipe slots per modular product)
 #   class 0 (p < 2^30, Mont32): fmaheavy pipe, 64 IMAD/clk/SM (guide: rt_SMSP = 2);
 #            IMAD.WIDE 2 + IMAD 1 + IMAD.HI 2 = 5 slots per product (WIDE/HI measured at half rate)
@@ -303,7 +305,19 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     pipe, lanes, slots = ROOF[cls]
     peak_mulmod = lanes * sms * mhz * 1e6 / slots
-    achieved = MULMODS_PER_TERM * k_terms / (k_ms / 1e3) if k_ms > 0 else 0.0
+    # achieved = SURVEY 8(d) per-unit figure x units: 2 mulmods x (227/6480 p [W] + 27/512 p [V]) summed over
+    # the primes of the dominant kernel's class, / that kernel's time (executed terms reported alongside)
+    pr = ds.primes[: ds.n_primes]
+    lim = {0: (0, 1 << 30), 1: (1 << 30, 1 << 44), 2: (1 << 44, 1 << 62)}[cls]
+    sel = pr[(pr >= lim[0]) & (pr < lim[1])]
+    sum_p = float(sel.double().sum().item()) if sel.numel() else 0.0
+    if world > 1:
+        t_sp = torch.tensor([sum_p], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_sp)
+        sum_p = float(t_sp.item())
+    alg_terms = sum(TERMS_PER_P[t] * sum_p for t in (1, 2) if w.mode & t)
+    achieved = MULMODS_PER_TERM * alg_terms / (k_ms / 1e3) if k_ms > 0 else 0.0
+    executed = MULMODS_PER_TERM * k_terms / (k_ms / 1e3) if k_ms > 0 else 0.0
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"r1_{args.workload}_residue_kernel_full.txt")
     if os.path.exists(prof):
@@ -319,6 +333,8 @@ def main():
     kname = {0: "residue_kernel<Mont32> (class 0, p < 2^30)", 1: "residue_kernel<Mont64, FP64 engine> (class 1)",
              2: "residue_kernel<Mont64> (class 2, p >= 2^44)"}[cls]
     roof = {"bound": "alu", "kernel": kname, "achieved": achieved / 1e9, "peak": peak_mulmod / 1e9,
+            "achieved_basis": "SURVEY.md 8(d): 2 mulmods x (227/6480 p + 27/512 p) per prime (BB30/EE33 work)",
+            "executed_gmulmod_s": executed / 1e9,
             "unit": "Gmulmod/s", "frac": achieved / peak_mulmod if peak_mulmod else None, "traffic": traffic,
             "traffic_unit": "bytes/launch (DRAM read+write, ncu --set full, profiles/)",
             "peak_basis": f"{pipe} pipe: {lanes} lanes/clk/SM x {sms} SMs x {mhz:.0f} MHz ({peak_kind} sm_max_mhz) "
