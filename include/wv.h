@@ -21,7 +21,8 @@
  * Conventions for every entry point:
  *  - integers are host-endian; residues are canonical in [0, p);
  *    WV_RES_NONE marks a test that was not requested;
- *  - ranges are half-open [lo, hi); primes < 5 are skipped; hi <= 2^62;
+ *  - ranges are half-open [lo, hi); primes < 5 are skipped; hi <= 2^62; one call handles
+ *    windows with fewer than 2^32 primes (WV_EINVAL otherwise: sweep in blocks);
  *  - outputs are sorted ascending by p and identical for every shard count,
  *    block size and internal partition (the combine is exact);
  *  - the library never keeps caller pointers after a call returns;

@@ -348,7 +348,7 @@ static void layout_tail(Layout &L) {
 }
 
 static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, uint32_t nshards, uint64_t block,
-                       Layout &L) {
+                       Layout &L, bool records = true) {
     if (hi <= lo) return set_err(WV_EINVAL, "empty or inverted range [%llu, %llu)", (unsigned long long)lo,
                                  (unsigned long long)hi);
     if (hi > WV_HI_MAX) return set_err(WV_EINVAL, "hi > 2^62");
@@ -384,6 +384,9 @@ static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, 
         cap += prime_bound(be - bs);
     }
     L.prime_cap = cap;
+    if (records && cap >= (1ull << 32))   // record indices are 32-bit: split such windows into blocks / sweeps
+        return set_err(WV_EINVAL, "window holds up to %llu primes (> 2^32): use smaller windows or wv_search_shard",
+                       (unsigned long long)cap);
     L.K = cap * L.ntests;
     // base primes: q <= isqrt(hi - 1)
     const uint64_t r = isqrt64(hi - 1);
@@ -796,7 +799,7 @@ extern "C" int wv_near_misses_device(const uint64_t *d_primes, const uint64_t *d
 
 extern "C" int wv_prime_count(uint64_t lo, uint64_t hi, uint64_t *count) {
     Layout L;
-    TRY(make_layout(lo, hi, 1, 0, 1, 0, L));
+    TRY(make_layout(lo, hi, 1, 0, 1, 0, L, false));
     DevCtx *c;
     TRY(ctx_get(&c));
     cudaStream_t st = c->stream;
