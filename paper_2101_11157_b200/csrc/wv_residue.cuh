@@ -494,6 +494,11 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const War
                     }
                 }
             }
+            if (PAIRS && i + 2 <= kk) {                // remainder: at most one pair + one single step
+                #pragma unroll
+                for (int s_ = 0; s_ < S; s_++) run[s_].step2(mo, md);
+                i += 2;
+            }
             for (; i < kk; i++) {
                 #pragma unroll
                 for (int s_ = 0; s_ < S; s_++) run[s_].step(mo, md);
