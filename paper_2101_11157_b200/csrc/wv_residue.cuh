@@ -301,11 +301,14 @@ struct Run {
     }
     __device__ __forceinline__ void reduce(const ModD &) {}
     __device__ __forceinline__ void result(const M &, const ModD &, W &c0, W &c1) const { c0 = a0; c1 = a1; }
-    // sum-start state (u, d1, d2) to / from shared memory, and a1 <- a1 * ratio (Montgomery form)
+    // sum-start state (u, d1, d2) to / from shared memory; coefficient rescaling at a sum switch
     __device__ __forceinline__ void save_start(uint64_t *st) const { st[0] = u; st[1] = d1; st[2] = d2; }
     __device__ __forceinline__ void load_start(const uint64_t *st) { u = (W)st[0]; d1 = (W)st[1]; d2 = (W)st[2]; }
-    __device__ __forceinline__ void scale1(const M &mo, const ModD &, uint64_t ratio_m, uint64_t) {
-        a1 = mo.mul(a1, (W)ratio_m);
+    // cross from sum j to j+1: keep V = a_{j+1} a1 / a0 by a1 <- a_j a1, a0 <- a_{j+1} a0
+    __device__ __forceinline__ void scale2(const M &mo, const ModD &, uint64_t cj_m, uint64_t cn_m, uint64_t,
+                                           uint64_t) {
+        a1 = mo.mul(a1, (W)cj_m);
+        a0 = mo.mul(a0, (W)cn_m);
     }
 };
 
@@ -364,8 +367,10 @@ struct RunD {
         d1 = __longlong_as_double((long long)st[1]);
         d2 = __longlong_as_double((long long)st[2]);
     }
-    __device__ __forceinline__ void scale1(const M &, const ModD &md, uint64_t, uint64_t ratio_canon) {
-        a1 = md.mul(a1, (double)ratio_canon);   // |a1| <= 2p, ratio < p: |result| <= p
+    __device__ __forceinline__ void scale2(const M &, const ModD &md, uint64_t, uint64_t, uint64_t cj_c,
+                                           uint64_t cn_c) {
+        a1 = md.mul(a1, (double)cj_c);          // |a1| <= 2p, coefficient < p: |result| <= p
+        a0 = md.mul(a0, (double)cn_c);
     }
 };
 
@@ -395,13 +400,14 @@ struct WarpTab {
     uint64_t cum[MAX_CONTIG_M + 1];     // prefix counts (flattened term space)
     uint64_t coef[MAX_CONTIG_M];        // a_j mod p, Montgomery form
     uint64_t st[MAX_CONTIG_M][3];       // run state (u, d1, d2) at s = first_j
-    uint64_t ratio[MAX_CONTIG_M];       // a_j / a_{j+1}: Montgomery form (IMAD) or canonical (FP64)
+    uint64_t coefc[MAX_CONTIG_M];       // a_j mod p, canonical (FP64 engine)
     uint32_t cont;                      // 1: every a_j is a unit mod p -> continuous runs across sums
 };
 
-// Fill st[] and ratio[] (warp-cooperative) for the continuous switch: a stream that leaves sum j
-// at its end enters sum j+1 at its start, so it loads that sum's start state and rescales
-// a1 by a_j / a_{j+1}: the running pair then represents sum_j a_j S_j / a_{j+1} without a merge.
+// Fill st[] (and coefc[]) warp-cooperatively for the continuous switch: a stream that leaves
+// sum j at its end enters sum j+1 at its start, so it loads that sum's start state and keeps
+// V = a_{j+1} a1 / a0 invariant by a1 <- a_j a1, a0 <- a_{j+1} a0 -- no merge, no re-seed and
+// no modular inverse.  Requires every a_j to be a unit mod p (else tab.cont = 0: merge path).
 template <class M, class R>
 __device__ __forceinline__ void prepare_switch(const M &mo, const ModD &md, WarpTab &tb, uint32_t m) {
     using W = typename M::W;
@@ -411,27 +417,12 @@ __device__ __forceinline__ void prepare_switch(const M &mo, const ModD &md, Warp
         R tmp;
         tmp.setup(mo, md, tb.first[j]);
         tmp.save_start(tb.st[j]);
-        unit = unit && mo.canon((W)tb.coef[j]) != 0;
+        const uint64_t cc = mo.canon((W)tb.coef[j]);
+        tb.coefc[j] = cc;
+        unit = unit && cc != 0;
     }
     const bool all = __all_sync(0xffffffffu, unit);
     if (lane == 0) tb.cont = all ? 1u : 0u;
-    if (all) {
-        W inv[3];
-        uint32_t k = 0;
-        for (uint32_t j = lane; j < m; j += 32, k++) inv[k] = mont_inv(mo, (W)tb.coef[j]);
-        __syncwarp();
-        k = 0;
-        for (uint32_t j = lane; j < m; j += 32, k++) tb.ratio[j] = inv[k];     // stash 1/a_j
-        __syncwarp();
-        W rr[3];
-        k = 0;
-        for (uint32_t j = lane; j < m; j += 32, k++)
-            rr[k] = (j + 1 < m) ? mo.mul((W)tb.coef[j], (W)tb.ratio[j + 1]) : (W)0;
-        __syncwarp();
-        k = 0;
-        for (uint32_t j = lane; j < m; j += 32, k++)
-            tb.ratio[j] = R::kFP ? mo.canon(rr[k]) : (uint64_t)rr[k];
-    }
     __syncwarp();
 }
 
@@ -522,7 +513,7 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const War
                 if (cont && t[i] < te[i]) {
                     // continuous switch: enter the next non-empty sum at its start
                     do {
-                        run[i].scale1(mo, md, tab.ratio[j[i]], tab.ratio[j[i]]);
+                        run[i].scale2(mo, md, tab.coef[j[i]], tab.coef[j[i] + 1], tab.coefc[j[i]], tab.coefc[j[i] + 1]);
                         j[i]++;
                     } while (cum[j[i] + 1] <= t[i]);
                     run[i].load_start(tab.st[j[i]]);
