@@ -167,7 +167,7 @@ static int set_err(int code, const char *fmt, ...) {
 // (prime class, engine, streams per lane for e = 2 / e = 3 sums); selected per class by the
 // env vars WV_VARIANT0/1/2 (index into this table) for benchmarking; defaults below.
 typedef void (*ResKern)(const Rec *, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, ulonglong2 *,
-                        unsigned long long *, uint32_t);
+                        unsigned long long *, uint32_t, const uint32_t *, uint32_t);
 typedef void (*LaneKern)(const Rec *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
                          uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *);
 struct Variant { const char *name; int cls; ResKern fn; LaneKern lane; };
@@ -327,6 +327,8 @@ struct Layout {
            o_flags, o_pos, o_kb, o_gq, o_gstart, total;
     uint64_t ngt;           // lane-mode group-tests: ceil(prime_cap / 32) * ntests
     uint64_t tiles_n;
+    uint32_t segstride;     // coarse seg-chunk index entries per record (0: none)
+    size_t o_segidx;
 };
 
 static void layout_tail(Layout &L) {
@@ -344,7 +346,28 @@ static void layout_tail(Layout &L) {
     if (ntiles(L.ngt + 1) > t) t = ntiles(L.ngt + 1);
     if (L.tiles_n < t) L.tiles_n = t;
     L.o_tiles = o; o += al(L.tiles_n * 8);
+    L.o_segidx = o; o += al(L.K * L.segstride * 4);   // last: a stride-0 layout is a prefix of this one
     L.total = o;
+}
+
+// Entries of the coarse seg-chunk index per record: max ceil(m / 32) over the sum-aligned (seg)
+// congruences the current schedule (tiers + overrides) can pick for primes below hi.
+static uint32_t seg_stride(uint64_t hi) {
+    const Table &T = table();
+    uint32_t s = 0;
+    auto consider = [&](int id) {
+        if (id >= 0 && id < (int)T.hdr.size() && T.hdr[id].seg) {
+            const uint32_t r = (T.hdr[id].m + 31) / 32;
+            if (r > s) s = r;
+        }
+    };
+    for (int t = 0; t < 2; t++) {
+        const int force = t == 0 ? g_sched.w_force : g_sched.v_force;
+        if (force >= 0) { consider(force); continue; }
+        for (int i = 0; i < g_sched.n[t]; i++)
+            if (i == 0 || g_sched.th[t][i] < hi) consider(g_sched.id[t][i]);
+    }
+    return s;
 }
 
 static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, uint32_t nshards, uint64_t block,
@@ -409,6 +432,7 @@ static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, 
     L.o_pos = o;    o += al((L.prime_cap + 1) * 8);
     L.tiles_n = ntiles(nsegmax + 1);
     L.total = o;
+    L.segstride = records ? seg_stride(hi) : 0;
     layout_tail(L);
     return WV_OK;
 }
@@ -477,6 +501,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     uint64_t *tiles = (uint64_t *)WS(ws, L.o_tiles);
     uint64_t *gq = (uint64_t *)WS(ws, L.o_gq);
     uint64_t *gstart = (uint64_t *)WS(ws, L.o_gstart);
+    uint32_t *segidx = L.segstride ? (uint32_t *)WS(ws, L.o_segidx) : nullptr;
     read_variant_env();
     int var0 = g_variant[0];
     bool lane = sorted && kVariants[var0].lane != nullptr;
@@ -496,7 +521,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             (void)table();
             LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
                    nch, (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
-                   (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr);
+                   (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr, segidx, L.segstride);
         }
         TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
         if (lane) TRY(scan_excl<uint64_t>(gq, L.ngt, gstart, gstart + L.ngt, tiles, st));
@@ -571,7 +596,8 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             unsigned long long *cnt = (unsigned long long *)(misc + M_CNT + cls);
             const int var = cls == 0 ? var0 : g_variant[cls];
             const unsigned grid = c->sms * c->occ[var];
-            LAUNCH(kVariants[var].fn, grid, RES_THREADS, st, recs, start, ka, kz, a_, b_, glo, part, cnt, 1u << cls);
+            LAUNCH(kVariants[var].fn, grid, RES_THREADS, st, recs, start, ka, kz, a_, b_, glo, part, cnt, 1u << cls,
+                   segidx, L.segstride);
             if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         const uint64_t nrec = khi - klo;
@@ -674,34 +700,43 @@ extern "C" int wv_search_device(uint64_t lo, uint64_t hi, uint32_t mode, uint32_
     return rc;
 }
 
-extern "C" int wv_residues_workspace_bytes(size_t n, uint64_t max_p, uint32_t mode, size_t *workspace_bytes) {
-    (void)max_p;
-    if (mode < 1 || mode > 3) return set_err(WV_EINVAL, "mode %u not in {1,2,3}", mode);
-    Layout L;
+// residues-only layout; the coarse seg index is sized for primes <= max_p
+static void residues_layout(size_t n, uint64_t max_p, uint32_t mode, Layout &L) {
     memset(&L, 0, sizeof L);
     L.mode = mode;
     L.ntests = mode == 3 ? 2 : 1;
     L.prime_cap = n;
     L.K = (uint64_t)n * L.ntests;
+    L.hi = max_p < WV_HI_MAX ? max_p + 1 : WV_HI_MAX;
     L.o_misc = 0;
     L.total = al(M_SLOTS * 8);
     L.tiles_n = 1;
+    L.segstride = seg_stride(L.hi);
     layout_tail(L);
+}
+
+extern "C" int wv_residues_workspace_bytes(size_t n, uint64_t max_p, uint32_t mode, size_t *workspace_bytes) {
+    if (mode < 1 || mode > 3) return set_err(WV_EINVAL, "mode %u not in {1,2,3}", mode);
+    Layout L;
+    residues_layout(n, max_p, mode, L);
     if (workspace_bytes) *workspace_bytes = L.total;
     return WV_OK;
 }
 
 extern "C" int wv_residues_device(const uint64_t *d_primes, size_t n, uint32_t mode, uint64_t *d_res_w,
                                   uint64_t *d_res_v, void *d_workspace, size_t workspace_bytes, void *stream) {
-    size_t need;
-    TRY(wv_residues_workspace_bytes(n, 0, mode, &need));
+    if (mode < 1 || mode > 3) return set_err(WV_EINVAL, "mode %u not in {1,2,3}", mode);
     if (n == 0) return WV_OK;
     if (!d_primes || !d_res_w || !d_res_v) return set_err(WV_EINVAL, "null pointer");
+    // the largest coarse seg index that fits the caller's workspace (a smaller layout is a prefix)
     Layout L;
-    memset(&L, 0, sizeof L);
-    L.mode = mode; L.ntests = mode == 3 ? 2 : 1; L.prime_cap = n; L.K = (uint64_t)n * L.ntests;
-    L.o_misc = 0; L.total = al(M_SLOTS * 8); L.tiles_n = 1;
-    layout_tail(L);
+    residues_layout(n, WV_HI_MAX, mode, L);
+    if (d_workspace && workspace_bytes < L.total) {
+        for (uint64_t mp : {(uint64_t)1 << 40, (uint64_t)1 << 33, (uint64_t)1 << 29, (uint64_t)5}) {
+            residues_layout(n, mp, mode, L);
+            if (workspace_bytes >= L.total) break;
+        }
+    }
     cudaStream_t st = (cudaStream_t)stream;
     void *ws = d_workspace;
     if (ws && workspace_bytes < L.total) return set_err(WV_ENOSPC, "workspace %zu < %zu", workspace_bytes, L.total);

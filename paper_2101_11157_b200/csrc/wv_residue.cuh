@@ -125,7 +125,8 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
                             uint64_t n_primes_host, uint64_t kmax, uint32_t mode, Sched sched,
                             Rec *__restrict__ recs, uint64_t *__restrict__ nchunks,
                             unsigned long long *__restrict__ first64, int *__restrict__ err,
-                            unsigned long long *__restrict__ terms, uint64_t *__restrict__ gq) {
+                            unsigned long long *__restrict__ terms, uint64_t *__restrict__ gq,
+                            uint32_t *__restrict__ segidx, uint32_t segstride) {
     const uint32_t ntests = (mode == 3) ? 2 : 1;
     const uint64_t n = n_primes_dev ? *n_primes_dev : n_primes_host;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kmax;
@@ -152,9 +153,12 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         if (L > 0x40000000ull) L = 0x40000000ull;
         uint64_t nc = (T + 32 * L - 1) / (32 * L);
         if (c.seg) {                                   // sum-aligned chunks: ceil(n_j / CT) per sum
+            // coarse index (when the stride holds it): segidx[k * segstride + r] = chunks of sums < 32 r
             const uint64_t CT = 32 * L;
+            const bool idx = segidx && (c.m + 31) / 32 <= segstride;
             nc = 0;
             for (uint32_t j = 0; j < c.m; j++) {
+                if (idx && (j & 31) == 0) segidx[k * segstride + (j >> 5)] = (uint32_t)nc;
                 uint64_t f, cnt;
                 sum_bounds(p, c_terms[c.off + j], &f, &cnt);
                 nc += (cnt + CT - 1) / CT;
@@ -547,7 +551,8 @@ template <class M, int CLASS, int ENGINE, int S2, int S3, bool PAIRS = false>
 __global__ void __launch_bounds__(RES_THREADS, (ENGINE == 0 && CLASS == 0) ? 1 : 3)
 residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
                uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
-               unsigned long long *__restrict__ counter, uint32_t class_mask) {
+               unsigned long long *__restrict__ counter, uint32_t class_mask,
+               const uint32_t *__restrict__ segidx, uint32_t segstride) {
     using W = typename M::W;
     __shared__ WarpTab s_tab[RES_WARPS];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -570,10 +575,22 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
         uint64_t t0, t1;
         if (cg.seg) {
             // sum-aligned chunk: locate (sum js, chunk cc) of local chunk c by a warp scan of
-            // ceil(n_j / CT) over the sums, 32 sums per round
+            // ceil(n_j / CT) over the sums, 32 sums per round, starting at the block of 32 sums
+            // the plan kernel's coarse index places c in (entries nondecreasing: count them <= c)
             uint64_t carry = 0, sf = 0, sn = 0, cc = 0;
-            uint32_t js = 0;
-            for (uint32_t base = 0; base < m; base += 32) {
+            uint32_t js = 0, base0 = 0;
+            const uint32_t R = (m + 31) / 32;
+            if (segidx && R <= segstride) {
+                const uint32_t *ix = segidx + k * segstride;
+                uint32_t cntle = 0;
+                for (uint32_t rr = 0; rr < R; rr += 32) {
+                    const bool le = rr + lane < R && (uint64_t)ix[rr + lane] <= c;
+                    cntle += __popc(__ballot_sync(0xffffffffu, le));
+                }
+                base0 = (cntle - 1) * 32;                 // entry 0 is 0 <= c
+                carry = ix[cntle - 1];
+            }
+            for (uint32_t base = base0; base < m; base += 32) {
                 const uint32_t jj = base + lane;
                 uint64_t f = 0, n = 0;
                 if (jj < m) sum_bounds(r.p, tb[jj], &f, &n);
