@@ -189,6 +189,7 @@ static const Variant kVariants[] = {
     {"c2 int s1/1 pairs", 2, residue_kernel<Mont64, 2, 0, 1, 1, true>, nullptr},
 };
 static const int NVAR = sizeof kVariants / sizeof kVariants[0];
+static_assert(NVAR <= 32, "DevCtx::occ holds 32 variants");
 static const int kDefaultVariant[3] = {13, 6, 8};  // measured best (scripts/variant_sweep.py)
 static int g_variant[3] = {13, 6, 8};              // per class
 static const int kChunkFallback0 = 13;             // class-0 chunk variant when lane mode is unusable
@@ -209,7 +210,7 @@ static void read_variant_env() {
 struct DevCtx {
     bool ready = false;
     int sms = 0;
-    int occ[16] = {};            // residue-kernel blocks per SM per kernel variant
+    int occ[32] = {};            // residue-kernel blocks per SM per kernel variant
     uint32_t *d_base0 = nullptr;   // odd primes < 65536
     uint32_t nbase0 = 0;
     cudaStream_t stream = nullptr; // internal stream for the host-buffer API
