@@ -250,6 +250,44 @@ int wv_stats_reset(void);
 int wv_kernel_variant_info(int id, char *name, size_t name_cap, int *cls);
 int wv_set_kernel_variant(int cls, int id);
 
+/* ------------------------------------------- general-index residues (NEXT-3)
+ * The irregular-pair census of P:L88-103: for every prime p in [lo, hi)
+ * (p >= 5, hi <= 2^30) and every even index 2 <= 2k <= p-3,
+ *   B_{2k} mod p  (mode bit 1) from eqnSV for general k,
+ *       C_k(3,4,6) B_{2k} == S_{2k-1}(1/6, 1/4)  (mod p),
+ *       C_k(a,b,c) = (a^{p-2k} + b^{p-2k} - c^{p-2k} - 1)/(4k);
+ *     where C_k(3,4,6) == 0 (mod p), from the first of VOR (2,3,4),
+ *     (4,5,8), eqnVandiver, eqnTW1 b = 2, 4, 6, 7,
+ *     8, 9, ... whose C_k is a unit (WV_ECUDA "no unit C_k" if
+ *     none up to b = 1031: not seen for any p < 30000, where b <= 28 suffices);
+ *   E_{2k} mod p  (mode bit 2, secant convention) from eqnE1
+ *     read as  (-1)^j 4^{2j-1} E_{p-1-2j} == S_{p-1-2j}(0, 1/4)  (reading R10,
+ *     the printed sign (-1)^{(p-1)/2-j} is wrong for half the j).
+ * All exponents of a prime are evaluated together by a walk over the
+ * multiplicative group (powers of a primitive root): (p-1)/2 Montgomery
+ * products per index, i.e. ~p^2/2 per prime for both kinds -- a census
+ * workload for p up to ~10^6, not for the frontier primes.
+ *
+ * wv_census: p | B_{2k} ("irregular pair (p, 2k)", kind 1) and p | E_{2k}
+ * ("E-irregular pair", kind 2) into out[0..cap), sorted by (p, kind, index);
+ * *n_pairs = their number (WV_ENOSPC if > cap, nothing written past cap);
+ * *n_primes = primes in the window; *checksum = sum mod 2^64 over every
+ * computed (p, index, kind, residue) of wv_census_checksum_term.  Any
+ * out-pointer may be NULL.  Runs on the library's device stream; synchronous.
+ * Errors: WV_EINVAL (lo >= hi, hi > 2^30, mode not in {1,2,3}), WV_ENOMEM,
+ * WV_ECUDA. */
+typedef struct { uint64_t p; uint32_t index; uint32_t kind; } wv_pair;
+int wv_census(uint64_t lo, uint64_t hi, uint32_t mode, wv_pair *out, size_t cap, size_t *n_pairs,
+              size_t *n_primes, uint64_t *checksum);
+/* wv_census_residues: the residues themselves, one record per (p, index),
+ * p ascending then index = 2, 4, ..., p-3; res_b / res_e = UINT64_MAX for a
+ * kind not requested.  *n = sum over primes of (p-3)/2; WV_ENOSPC (nothing
+ * computed) if cap < *n. */
+typedef struct { uint64_t p; uint32_t index; uint32_t reserved; uint64_t res_b; uint64_t res_e; } wv_index_residue;
+int wv_census_residues(uint64_t lo, uint64_t hi, uint32_t mode, wv_index_residue *out, size_t cap, size_t *n);
+/* mix64(p ^ (index << 32) ^ rotl(res, 17) ^ (kind << 62)), mix64 = splitmix64 finaliser */
+uint64_t wv_census_checksum_term(uint64_t p, uint32_t index, uint32_t kind, uint64_t res);
+
 /* Counters: kernels launched by this library since load (process-wide). */
 uint64_t wv_launch_count(void);
 /* Library / device info string (build flags, sm, ...). */

@@ -9,7 +9,9 @@ module only compiles/loads it and marshals arguments.
 Tiers (see wv_oracle.c for the cited passages):
 
 * tier A  -- definitions: Bernoulli recurrence / secant recurrence mod p,
-  O(p^2), used for p <= 2000 (and in pins up to a few 10^4);
+  O(p^2), used for p <= 2000 (and in pins up to a few 10^4); it yields every
+  index 2k <= p-3 at once, so it is also the oracle of the general-index census
+  (``index_residues``, SURVEY.md 8(f) NEXT-3);
 * tier B  -- W: sum_{k<p} k^-2 mod p^2 (eqnWolst + Glaisher), p < 2^32;
   V: Glaisher's quarter sum, -4 E_{p-3} == sum_{s<p/4} s^-2 (DESIGN.md R1);
 * tier C  -- W for p >= 2^32: Stafford-Vandiver eqnSV == eqnBB1
@@ -179,3 +181,34 @@ def residues(plist, mode: int = 3, workers: int | None = None):
     _load()
     with ProcessPoolExecutor(max_workers=workers) as ex:
         return list(ex.map(_one, [(p, mode) for p in plist], chunksize=max(1, len(plist) // (workers * 16))))
+
+
+# ---------------------------------------------------------------- general indices (NEXT-3)
+def index_residues(p: int):
+    """Tier A for every even index (the irregular-pair census): lists
+    (index, B_index mod p, E_index mod p) for index = 2, 4, ..., p-3, straight from the
+    recurrences of the generating functions (bernoulli_mod_p / euler_mod_p)."""
+    B = bernoulli_mod_p(p, p - 3)
+    E = euler_mod_p(p, p - 3)
+    return [(i, B[i], E[i // 2]) for i in range(2, p - 2, 2)]
+
+
+def _index_one(p):
+    return p, index_residues(p)
+
+
+def index_residues_many(plist, workers: int | None = None):
+    """{p: index_residues(p)} over a list of primes (process pool)."""
+    plist = list(plist)
+    workers = workers or os.cpu_count() or 1
+    if workers == 1 or len(plist) < 2:
+        return dict(_index_one(p) for p in plist)
+    _load()
+    with ProcessPoolExecutor(max_workers=workers) as ex:
+        return dict(ex.map(_index_one, plist, chunksize=1))
+
+
+def irregular_pairs(p: int):
+    """([2k: p | B_2k], [2k: p | E_2k]) for 2 <= 2k <= p-3 ((E-)irregular pairs)."""
+    r = index_residues(p)
+    return [i for i, b, _ in r if b == 0], [i for i, _, e in r if e == 0]

@@ -16,4 +16,4 @@ the secant convention (mode V).  ``workloads`` holds the BASELINE configs.
 from ._wv import (NEAR_DTYPE, near_misses_device, HIT_DTYPE, HIT_V, HIT_W, MODE_BOTH, MODE_V, MODE_W, RES_DTYPE, RES_NONE, DeviceSearch,  # noqa: F401
                   WVError, checksum_term, congruences, launch_count, lib, prime_count, residues_device, residues_of, schedule,
                   search, search_shard, shard_blocks, pinned_buffers, set_schedule_override, sieve_device, kernel_variants, set_kernel_variant, stats, stats_enable, stats_reset,
-                  version)
+                  version, census, census_residues, census_checksum_term, PAIR_DTYPE, IDXRES_DTYPE, KIND_B, KIND_E)

@@ -23,6 +23,9 @@ HIT_W, HIT_V = 1, 2
 HIT_DTYPE = np.dtype([("p", "<u8"), ("flags", "<u4"), ("reserved", "<u4")])
 RES_DTYPE = np.dtype([("p", "<u8"), ("res_w", "<u8"), ("res_v", "<u8")])
 NEAR_DTYPE = np.dtype([("p", "<u8"), ("symres", "<i8"), ("test", "<u4"), ("reserved", "<u4")])
+PAIR_DTYPE = np.dtype([("p", "<u8"), ("index", "<u4"), ("kind", "<u4")])        # kind 1: p | B_index, 2: E
+IDXRES_DTYPE = np.dtype([("p", "<u8"), ("index", "<u4"), ("reserved", "<u4"), ("res_b", "<u8"), ("res_e", "<u8")])
+KIND_B, KIND_E = 1, 2
 
 
 class WVError(RuntimeError):
@@ -86,6 +89,9 @@ SIGNATURES = {
     "wv_stats_reset": (_i, []),
     "wv_kernel_variant_info": (_i, [_i, ctypes.c_char_p, _sz, _P(_i)]),
     "wv_set_kernel_variant": (_i, [_i, _i]),
+    "wv_census": (_i, [_u64, _u64, _u32, _vp, _sz, _P(_sz), _P(_sz), _P(_u64)]),
+    "wv_census_residues": (_i, [_u64, _u64, _u32, _vp, _sz, _P(_sz)]),
+    "wv_census_checksum_term": (_u64, [_u64, _u32, _u32, _u64]),
     "wv_launch_count": (_u64, []),
     "wv_version": (ctypes.c_char_p, []),
     "wv_last_error": (ctypes.c_char_p, []),
@@ -300,6 +306,35 @@ def shard_blocks(lo, hi, shard, nshards, block=0):
 # ------------------------------------------------------------------ small utilities
 def checksum_term(p, rw, rv):
     return int(lib().wv_checksum_term(p, rw, rv))
+
+
+def census(lo: int, hi: int, mode: int = MODE_BOTH, cap: int = 1 << 16):
+    """Irregular (kind 1) and E-irregular (kind 2) pairs of the primes in [lo, hi) (NEXT-3):
+    (pairs[PAIR_DTYPE] sorted by (p, kind, index), n_primes, checksum)."""
+    n, npr, chk = _sz(), _sz(), _u64()
+    out = np.zeros(cap, dtype=PAIR_DTYPE)
+    rc = lib().wv_census(lo, hi, mode, out.ctypes.data, cap, ctypes.byref(n), ctypes.byref(npr), ctypes.byref(chk))
+    if rc == WV_ENOSPC:
+        out = np.zeros(n.value, dtype=PAIR_DTYPE)
+        rc = lib().wv_census(lo, hi, mode, out.ctypes.data, n.value, ctypes.byref(n), ctypes.byref(npr),
+                             ctypes.byref(chk))
+    _check(rc)
+    return out[: n.value], npr.value, chk.value
+
+
+def census_residues(lo: int, hi: int, mode: int = MODE_BOTH):
+    """B_{2k} / E_{2k} mod p for every prime in [lo, hi) and 2 <= 2k <= p-3 (IDXRES_DTYPE records)."""
+    n = _sz()
+    rc = lib().wv_census_residues(lo, hi, mode, None, 0, ctypes.byref(n))
+    if rc not in (WV_OK, WV_ENOSPC):
+        _check(rc)
+    out = np.zeros(n.value, dtype=IDXRES_DTYPE)
+    _check(lib().wv_census_residues(lo, hi, mode, out.ctypes.data if n.value else None, n.value, ctypes.byref(n)))
+    return out
+
+
+def census_checksum_term(p, index, kind, res):
+    return int(lib().wv_census_checksum_term(p, index, kind, res))
 
 
 def congruences():

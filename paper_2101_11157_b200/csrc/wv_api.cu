@@ -12,6 +12,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -21,6 +22,7 @@
 #include "wv_residue.cuh"
 #include "wv_scan.cuh"
 #include "wv_sieve.cuh"
+#include "wv_census.cuh"
 
 using namespace wv;
 
@@ -211,6 +213,7 @@ struct DevCtx {
     bool ready = false;
     int sms = 0;
     int occ[32] = {};            // residue-kernel blocks per SM per kernel variant
+    int occ_census = 1;          // census walk blocks per SM
     uint32_t *d_base0 = nullptr;   // odd primes < 65536
     uint32_t nbase0 = 0;
     cudaStream_t stream = nullptr; // internal stream for the host-buffer API
@@ -249,6 +252,8 @@ static int ctx_get(DevCtx **out) {
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[v], kVariants[v].lane, RES_THREADS, 0));
             if (c.occ[v] < 1) c.occ[v] = 1;
         }
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_census, census_walk_kernel, CEN_THREADS, 0));
+        if (c.occ_census < 1) c.occ_census = 1;
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         cudaMemPool_t pool;
         CK(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -1061,3 +1066,170 @@ extern "C" const char *wv_version(void) {
 }
 
 extern "C" const char *wv_last_error(void) { return g_err; }
+
+// ------------------------------------------------------------------ NEXT-3: index census
+// Sieve -> per-prime plan (primitive root, exponent and item counts) -> scans -> batches of
+// <= CEN_BUDGET index residues: walk, finalize, fix-up.  See wv_census.cuh and include/wv.h.
+static const uint64_t CEN_BUDGET = 1ull << 25;     // index residues per batch (acc: 256 MB)
+
+namespace {
+struct DevBufs {                                   // cudaFreeAsync on scope exit
+    cudaStream_t st;
+    std::vector<void *> v;
+    explicit DevBufs(cudaStream_t s) : st(s) {}
+    ~DevBufs() { for (void *p : v) cudaFreeAsync(p, st); cudaStreamSynchronize(st); }
+    template <typename T> int get(T **out, size_t n) {
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, n ? n * sizeof(T) : 1, st) != cudaSuccess)
+            return set_err(WV_ENOMEM, "cudaMallocAsync(%zu) failed", n * sizeof(T));
+        v.push_back(p);
+        *out = (T *)p;
+        return WV_OK;
+    }
+};
+}  // namespace
+
+static int census_impl(uint64_t lo, uint64_t hi, uint32_t mode, wv_pair *out, size_t cap, size_t *n_pairs,
+                       size_t *n_primes, uint64_t *checksum, wv_index_residue *out_res, size_t res_cap, size_t *n_res,
+                       bool want_res) {
+    static_assert(sizeof(wv_pair) == sizeof(CenPair), "wv_pair layout");
+    if (hi <= lo) return set_err(WV_EINVAL, "empty or inverted range [%llu, %llu)", (unsigned long long)lo,
+                                 (unsigned long long)hi);
+    if (hi > CEN_HI_MAX) return set_err(WV_EINVAL, "census needs hi <= 2^30");
+    if (mode < 1 || mode > 3) return set_err(WV_EINVAL, "mode %u not in {1,2,3}", mode);
+    DevCtx *c;
+    TRY(ctx_get(&c));
+    cudaStream_t st = c->stream;
+    const uint64_t lo5 = lo < 5 ? 5 : lo;
+    uint64_t n = 0;
+    DevBufs B(st);
+    uint64_t *d_primes = nullptr;
+    if (hi > lo5) {
+        const uint64_t pc = prime_bound(hi - lo5) + 1;
+        TRY(B.get(&d_primes, pc));
+        size_t nn = 0;
+        TRY(wv_sieve_device(lo5, hi, d_primes, pc, &nn, nullptr, 0, st));
+        n = nn;
+    }
+    if (n_primes) *n_primes = n;
+    std::vector<uint64_t> hp(n), heb(n + 1, 0), his(n + 1, 0);
+    if (n) CK(cudaMemcpy(hp.data(), d_primes, n * 8, cudaMemcpyDeviceToHost));
+    uint64_t nrec = 0;
+    for (uint64_t i = 0; i < n; i++) nrec += (hp[i] - 3) / 2;
+    if (n_res) *n_res = nrec;
+    if (want_res && nrec > 0 && (!out_res || res_cap < nrec))
+        return set_err(WV_ENOSPC, "cap %zu < %llu index residues", res_cap, (unsigned long long)nrec);
+    uint64_t chk = 0, npairs = 0;
+    std::vector<CenPair> hpairs;
+    if (n) {
+        uint32_t *d_g;
+        uint64_t *d_ne, *d_ni, *d_eb, *d_is, *d_tiles;
+        unsigned long long *d_misc;
+        TRY(B.get(&d_g, n));
+        TRY(B.get(&d_ne, n));
+        TRY(B.get(&d_ni, n));
+        TRY(B.get(&d_eb, n + 1));
+        TRY(B.get(&d_is, n + 1));
+        TRY(B.get(&d_tiles, ntiles(n + 1)));
+        TRY(B.get(&d_misc, 8));
+        CK(cudaMemsetAsync(d_misc, 0, 64, st));
+        const unsigned gp = (unsigned)((n + 127) / 128 < (uint64_t)c->sms * 8 ? (n + 127) / 128 : c->sms * 8);
+        LAUNCH(census_plan_kernel, gp, 128, st, d_primes, n, mode, d_g, d_ne, d_ni);
+        TRY(scan_excl<uint64_t>(d_ne, n, d_eb, d_eb + n, d_tiles, st));
+        TRY(scan_excl<uint64_t>(d_ni, n, d_is, d_is + n, d_tiles, st));
+        CK(cudaMemcpyAsync(heb.data(), d_eb, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(his.data(), d_is, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        // batches [i0, i1) of <= CEN_BUDGET index residues (at least one prime)
+        std::vector<uint64_t> cut{0};
+        uint64_t amax = 0;
+        while (cut.back() < n) {
+            const uint64_t i0 = cut.back();
+            uint64_t i1 = i0 + 1;
+            while (i1 < n && heb[i1 + 1] - heb[i0] <= CEN_BUDGET) i1++;
+            cut.push_back(i1);
+            if (heb[i1] - heb[i0] > amax) amax = heb[i1] - heb[i0];
+        }
+        unsigned long long *d_acc;
+        uint64_t *d_res = nullptr;
+        CenFix *d_fix;
+        CenPair *d_pairs;
+        const uint64_t fcap = amax / 8 + 1024, pcap = cap > 65536 ? cap : 65536;
+        TRY(B.get(&d_acc, amax));
+        if (want_res) TRY(B.get(&d_res, amax));
+        TRY(B.get(&d_fix, fcap));
+        TRY(B.get(&d_pairs, pcap));
+        std::vector<uint64_t> hres;
+        const uint64_t per = mode == 3 ? 2 : 1;          // walked exponents per index record
+        for (size_t b = 0; b + 1 < cut.size(); b++) {
+            const uint64_t i0 = cut[b], i1 = cut[b + 1], nE = heb[i1] - heb[i0];
+            CK(cudaMemsetAsync(d_acc, 0, nE * 8, st));
+            CK(cudaMemsetAsync(d_misc + 2, 0, 24, st));  // fix count, unresolved, walk counter
+            LAUNCH(census_walk_kernel, c->sms * c->occ_census, CEN_THREADS, st, d_primes, d_g, d_is, d_eb, i0, i1,
+                   mode, d_acc, d_misc + 4);
+            const unsigned gf = (unsigned)((nE + 255) / 256 < (uint64_t)c->sms * 16 ? (nE + 255) / 256 : c->sms * 16);
+            LAUNCH(census_finalize_kernel, gf, 256, st, d_primes, d_eb, i0, i1, mode, d_acc, d_res, d_pairs, pcap,
+                   d_fix, fcap, d_misc);
+            uint64_t hm[2] = {0, 0};
+            CK(cudaMemcpyAsync(hm, d_misc + 2, 16, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (hm[0] > fcap) return set_err(WV_ECUDA, "census fix-up queue overflow (%llu > %llu)",
+                                             (unsigned long long)hm[0], (unsigned long long)fcap);
+            if (hm[0]) {
+                const unsigned gx = (unsigned)((hm[0] * 32 + 255) / 256 < (uint64_t)c->sms * 8 ? (hm[0] * 32 + 255) / 256
+                                                                                                : c->sms * 8);
+                LAUNCH(census_fixup_kernel, gx, 256, st, d_primes, d_eb, i0, mode, d_fix, hm[0], d_res, d_pairs, pcap,
+                       d_misc);
+                CK(cudaMemcpyAsync(hm, d_misc + 3, 8, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (hm[0]) return set_err(WV_ECUDA, "census: %llu B indices with no unit C_k among the congruences",
+                                          (unsigned long long)hm[0]);
+            }
+            if (want_res) {
+                hres.resize(nE);
+                CK(cudaMemcpy(hres.data(), d_res, nE * 8, cudaMemcpyDeviceToHost));
+                uint64_t r = 0;
+                for (uint64_t i = 0; i < i0; i++) r += (hp[i] - 3) / 2;
+                for (uint64_t i = i0; i < i1; i++) {
+                    const uint64_t base = heb[i] - heb[i0], m = (hp[i] - 3) / 2;
+                    for (uint64_t j = 0; j < m; j++, r++) {
+                        wv_index_residue &o = out_res[r];
+                        o.p = hp[i]; o.index = (uint32_t)(2 * j + 2); o.reserved = 0;
+                        o.res_b = mode == 2 ? UINT64_MAX : hres[base + per * j];
+                        o.res_e = mode == 1 ? UINT64_MAX : hres[base + per * j + (mode == 3 ? 1 : 0)];
+                    }
+                }
+            }
+        }
+        uint64_t hm[2];
+        CK(cudaMemcpyAsync(hm, d_misc, 16, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        npairs = hm[0];
+        chk = hm[1];
+        const uint64_t got = npairs < pcap ? npairs : pcap;
+        hpairs.resize(got);
+        if (got) CK(cudaMemcpy(hpairs.data(), d_pairs, got * sizeof(CenPair), cudaMemcpyDeviceToHost));
+    }
+    if (checksum) *checksum = chk;
+    if (n_pairs) *n_pairs = npairs;
+    std::sort(hpairs.begin(), hpairs.end(), [](const CenPair &a, const CenPair &b) {
+        return a.p != b.p ? a.p < b.p : (a.kind != b.kind ? a.kind < b.kind : a.index < b.index);
+    });
+    if (out) memcpy(out, hpairs.data(), (hpairs.size() < cap ? hpairs.size() : cap) * sizeof(wv_pair));
+    if (npairs > cap && (out || cap)) return set_err(WV_ENOSPC, "cap %zu < %llu pairs", cap, (unsigned long long)npairs);
+    return WV_OK;
+}
+
+extern "C" int wv_census(uint64_t lo, uint64_t hi, uint32_t mode, wv_pair *out, size_t cap, size_t *n_pairs,
+                         size_t *n_primes, uint64_t *checksum) {
+    return census_impl(lo, hi, mode, out, cap, n_pairs, n_primes, checksum, nullptr, 0, nullptr, false);
+}
+
+extern "C" int wv_census_residues(uint64_t lo, uint64_t hi, uint32_t mode, wv_index_residue *out, size_t cap,
+                                  size_t *n) {
+    return census_impl(lo, hi, mode, nullptr, 0, nullptr, nullptr, nullptr, out, cap, n, true);
+}
+
+extern "C" uint64_t wv_census_checksum_term(uint64_t p, uint32_t index, uint32_t kind, uint64_t res) {
+    return cen_checksum_term(p, index, kind, res);
+}

@@ -1,0 +1,329 @@
+// wv_census.cuh -- SURVEY.md 8(f) NEXT-3: general-index residues B_{2k}, E_{2k} mod p for every
+// even index 2 <= 2k <= p-3 of every prime p in a window (the irregular / E-irregular pair census
+// of P:L88-103), on sm_100a.
+//
+// The paper's congruences hold for every k with p-1 not dividing 2k:
+//   B:  C_k(3,4,6) B_{2k} == S_{2k-1}(1/6, 1/4)                      eqnSV
+//   E:  (-1)^k 4^{2k-1} E_{p-1-2k} == S_{p-1-2k}(0, 1/4)             eqnE1   (reading R10)
+// with S_l(x, y) = sum_{xp<s<yp} s^l mod p and C_k(a,b,c) = (a^{p-2k} + b^{p-2k} - c^{p-2k} - 1)/(4k).
+// Finite differences do not apply to s^l for large l, so all exponents of one prime are walked
+// together over the multiplicative group: with g a primitive root and s_j = g^j,
+//     S_l(I) = sum_{0<=j<(p-1)/2} [s'_j in I] sigma_j (g^l)^j,   s'_j = min(s_j, p - s_j),
+// sigma_j = 1 if s'_j = s_j else (-1)^l (s_{j+(p-1)/2} = -s_j, so each pair {s, p-s} is visited
+// once).  One lane owns one exponent l: per step one Montgomery product w <- w g^l and a
+// predicated add; the membership code of s'_j is shared by the warp through shared memory.
+// Every index of a prime costs (p-1)/2 steps.
+//
+// Where C_k(3,4,6) == 0 (mod p) the finalize kernel queues (p, l) for a fix-up that evaluates the
+// first congruence of a fixed list with a unit C_k directly (per-term powers; rare: ~1/p of the B
+// indices): VOR (2,3,4) P:L245-249, (4,5,8) P:L263-268, eqnVandiver (2,5,6) P:L171-175, eqnTW1
+// with b = 2, 4, 6, 7, then b = 8, 9, ....
+#pragma once
+#include <stdint.h>
+#include "wv_mont.cuh"
+#include "wv_residue.cuh"
+
+namespace wv {
+
+constexpr uint32_t CEN_SEG = 8192;             // walk steps per work item
+constexpr uint32_t CEN_TG = 4;                 // exponent tiles (of 32) per work item
+constexpr uint32_t CEN_TW_BMAX = 1024;         // fix-up: eqnTW1 parameters b <= this
+constexpr uint32_t CEN_THREADS = 256;
+constexpr uint32_t CEN_WARPS = CEN_THREADS / 32;
+constexpr uint64_t CEN_HI_MAX = 1ull << 30;    // Mont32 lazy range
+
+// Montgomery power: b in Montgomery form, result in Montgomery form ([0, 2p))
+__device__ __forceinline__ uint32_t cen_pow(const Mont32 &mo, uint32_t b, uint64_t e) {
+    uint32_t r = mo.r1;
+    while (e) {
+        if (e & 1) r = mo.mul(r, b);
+        b = mo.mul(b, b);
+        e >>= 1;
+    }
+    return r;
+}
+
+// number of exponents per prime for the mode: 3 -> l = 1..p-3; 1 -> odd l (B); 2 -> even l (E)
+__host__ __device__ __forceinline__ uint64_t cen_nexp(uint64_t p, uint32_t mode) {
+    return mode == 3 ? p - 3 : (p - 3) / 2;
+}
+// exponent of enumeration position q (0-based)
+__device__ __forceinline__ uint64_t cen_exp(uint64_t q, uint32_t mode) {
+    return mode == 3 ? q + 1 : (mode == 1 ? 2 * q + 1 : 2 * q + 2);
+}
+
+// one thread per prime: primitive root (smallest g with g^{(p-1)/q} != 1 for all primes q | p-1),
+// number of exponents and of work items (groups of CEN_TG exponent tiles of 32 x walk segments
+// of CEN_SEG steps)
+__global__ void census_plan_kernel(const uint64_t *__restrict__ primes, uint64_t n, uint32_t mode,
+                                   uint32_t *__restrict__ groot, uint64_t *__restrict__ nexp,
+                                   uint64_t *__restrict__ nitems) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = (uint32_t)primes[i];
+        uint32_t q[10], nq = 0, m = p - 1;
+        for (uint32_t d = 2; d * d <= m; d += (d == 2 ? 1 : 2)) {
+            if (m % d == 0) {
+                q[nq++] = d;
+                while (m % d == 0) m /= d;
+            }
+        }
+        if (m > 1) q[nq++] = m;
+        Mont32 mo;
+        mo.init(p);
+        uint32_t g = 2;
+        for (;; g++) {
+            const uint32_t gm = mo.to(g);
+            bool ok = true;
+            for (uint32_t t = 0; t < nq && ok; t++) ok = mo.canon(cen_pow(mo, gm, (p - 1) / q[t])) != 1;
+            if (ok) break;
+        }
+        groot[i] = g;
+        const uint64_t ne = cen_nexp(p, mode);
+        const uint64_t half = (p - 1) / 2;
+        nexp[i] = ne;
+        nitems[i] = ((ne + 32 * CEN_TG - 1) / (32 * CEN_TG)) * ((half + CEN_SEG - 1) / CEN_SEG);
+    }
+}
+
+// membership code of s' = min(s, p - s) for one walk step:
+//   bit 0: s' in (p/6, p/4) and s' = s      (B, sigma = +1)
+//   bit 1: s' in (p/6, p/4) and s' = p - s  (B, sigma = (-1)^l = -1 for odd l)
+//   bit 2: s' in (0, p/4)                   (E, sigma = +1 for even l)
+__device__ __forceinline__ uint32_t cen_code(uint32_t s, uint32_t p) {
+    const uint32_t sp = s <= p - s ? s : p - s;
+    const bool neg = sp != s;
+    const bool q4 = 4ull * sp < p;
+    const bool inb = q4 && 6ull * sp > p;
+    return (inb ? (neg ? 2u : 1u) : 0u) | (q4 ? 4u : 0u);
+}
+
+// Persistent walk: each warp takes items (prime i, tile group, walk segment); lane = exponent.
+// acc[ebase[i] - ebase[i_lo] + q] += the segment's sum (canonical Montgomery form, < p per item).
+__global__ void __launch_bounds__(CEN_THREADS)
+census_walk_kernel(const uint64_t *__restrict__ primes, const uint32_t *__restrict__ groot,
+                   const uint64_t *__restrict__ istart, const uint64_t *__restrict__ ebase, uint64_t i_lo,
+                   uint64_t i_hi, uint32_t mode, unsigned long long *__restrict__ acc,
+                   unsigned long long *__restrict__ counter) {
+    __shared__ uint32_t s_code[CEN_WARPS][CEN_SEG / 8];     // 4-bit codes, 8 per word
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t g_lo = istart[i_lo], g_hi = istart[i_hi];
+    for (;;) {
+        unsigned long long gi = 0;
+        if (lane == 0) gi = atomicAdd(counter, 1ull);
+        gi = __shfl_sync(0xffffffffu, gi, 0);
+        const uint64_t g = g_lo + gi;
+        if (g >= g_hi) break;
+        const uint64_t i = find_rec_warp(istart, i_lo, i_hi, g);
+        const uint32_t p = (uint32_t)primes[i];
+        const uint64_t c = g - istart[i];
+        const uint32_t half = (p - 1) / 2;
+        const uint32_t nseg = (half + CEN_SEG - 1) / CEN_SEG;
+        const uint64_t tg = c / nseg;
+        const uint32_t seg = (uint32_t)(c % nseg);
+        const uint32_t j0 = seg * CEN_SEG;
+        const uint32_t len = half - j0 < CEN_SEG ? half - j0 : CEN_SEG;
+        Mont32 mo;
+        mo.init(p);
+        const uint32_t gm = mo.to(groot[i]);
+        // codes of s_j = g^j, j in [j0, j0 + len): lane writes words wd = lane, lane + 32, ...
+        // (8 codes each).  s is kept plain: mul(s, g R) = s g (mod p).
+        const uint32_t nw = (len + 7) / 8;
+        {
+            const uint32_t g256 = cen_pow(mo, gm, 256);
+            uint32_t s0 = (uint32_t)mo.canon(cen_pow(mo, gm, (uint64_t)j0 + 8 * lane));
+            for (uint32_t wd = lane; wd < nw; wd += 32) {
+                uint32_t s = s0, word = 0;
+                #pragma unroll
+                for (int b = 0; b < 8; b++) {
+                    if (8 * wd + b < len) word |= cen_code(s, p) << (4 * b);
+                    s = mo.mul(s, gm);
+                    s = s >= p ? s - p : s;
+                }
+                s_code[wid][wd] = word;
+                s0 = mo.mul(s0, g256);
+                s0 = s0 >= p ? s0 - p : s0;
+            }
+        }
+        __syncwarp();
+        const uint64_t ne = cen_nexp(p, mode);
+        for (uint32_t tt = 0; tt < CEN_TG; tt++) {
+            const uint64_t q = (tg * CEN_TG + tt) * 32 + lane;
+            if ((tg * CEN_TG + tt) * 32 >= ne) break;                 // warp-uniform
+            const bool valid = q < ne;
+            const uint64_t l = cen_exp(valid ? q : 0, mode);
+            const uint32_t h = cen_pow(mo, gm, l);                   // g^l
+            uint32_t w = cen_pow(mo, h, j0);                         // g^{l j0}
+            const uint32_t sh = (l & 1) ? 0u : 2u;                   // odd l: bits 0/1; even l: bit 2
+            uint32_t a = 0;                                          // lazy sum in [0, 2p)
+            for (uint32_t wd = 0; wd < nw; wd++) {
+                const uint32_t word = s_code[wid][wd] >> sh;
+                if (8 * wd + 8 <= len) {
+                    #pragma unroll
+                    for (uint32_t b = 0; b < 8; b++) {
+                        const uint32_t t = (word >> (4 * b)) & 3u;  // 0: none, 1: +w, 2: -w
+                        const uint32_t v = t == 0 ? 0u : (t == 1 ? w : mo.p2 - w);
+                        a = mo.add(a, v);
+                        w = mo.mul(w, h);
+                    }
+                } else {
+                    for (uint32_t b = 0; 8 * wd + b < len; b++) {
+                        const uint32_t t = (word >> (4 * b)) & 3u;
+                        const uint32_t v = t == 0 ? 0u : (t == 1 ? w : mo.p2 - w);
+                        a = mo.add(a, v);
+                        w = mo.mul(w, h);
+                    }
+                }
+            }
+            if (valid) {
+                const uint32_t r = a >= p ? a - p : a;
+                atomicAdd(acc + (ebase[i] - ebase[i_lo]) + q, (unsigned long long)r);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+struct CenPair { uint64_t p; uint32_t index; uint32_t kind; };   // = wv_pair
+struct CenFix { uint64_t i; uint64_t e; };                         // prime index, batch entry
+
+__host__ __device__ __forceinline__ uint64_t cen_checksum_term(uint64_t p, uint32_t index, uint32_t kind,
+                                                               uint64_t res) {
+    return mix64(p ^ ((uint64_t)index << 32) ^ rotl64(res, 17) ^ ((uint64_t)kind << 62));
+}
+
+// outputs of one index residue: residue array, zero -> pair list, checksum
+__device__ __forceinline__ void cen_emit(uint64_t p, uint32_t index, uint32_t kind, uint64_t res, uint64_t e,
+                                         uint64_t *__restrict__ res_out, CenPair *__restrict__ pairs,
+                                         uint64_t pair_cap, unsigned long long *__restrict__ misc) {
+    if (res_out) res_out[e] = res;
+    if (res == 0) {
+        const unsigned long long k = atomicAdd(misc + 0, 1ull);
+        if (k < pair_cap) pairs[k] = CenPair{p, index, kind};
+    }
+    atomicAdd(misc + 1, (unsigned long long)cen_checksum_term(p, index, kind, res));
+}
+
+// C_k(3,4,6) numerator 3^t + 4^t - 6^t - 1 (t = p - 2k), canonical
+__device__ __forceinline__ uint32_t cen_cnum(const Mont32 &mo, uint32_t a, uint32_t b, uint32_t c, uint64_t t) {
+    const uint32_t pa = cen_pow(mo, mo.to(a), t), pb = cen_pow(mo, mo.to(b), t), pc = cen_pow(mo, mo.to(c), t);
+    uint32_t x = mo.add(pa, pb);
+    x = mo.add(x, mo.p2 - (pc >= mo.p2 ? pc - mo.p2 : pc));
+    x = mo.add(x, mo.p2 - mo.r1);
+    return (uint32_t)mo.canon(x);
+}
+
+// one thread per batch entry e: residue from the walked sum
+//   odd l = 2k-1:  B_{2k} = S (4k) / (3^t + 4^t - 6^t - 1),  t = p - 2k     (eqnSV)
+//   even l = t:    E_t = (-1)^k 4^{-(2k-1)} S,  2k = p - 1 - t              (eqnE1, reading R10)
+__global__ void census_finalize_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ ebase,
+                                       uint64_t i_lo, uint64_t i_hi, uint32_t mode,
+                                       const unsigned long long *__restrict__ acc, uint64_t *__restrict__ res_out,
+                                       CenPair *__restrict__ pairs, uint64_t pair_cap, CenFix *__restrict__ fix,
+                                       uint64_t fix_cap, unsigned long long *__restrict__ misc) {
+    const uint64_t nE = ebase[i_hi] - ebase[i_lo];
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nE; e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = i_lo, hi = i_hi;                 // ebase[lo] - ebase[i_lo] <= e < ebase[hi] - ...
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (ebase[mid] - ebase[i_lo] <= e) lo = mid; else hi = mid;
+        }
+        const uint64_t i = lo;
+        const uint32_t p = (uint32_t)primes[i];
+        const uint64_t q = e - (ebase[i] - ebase[i_lo]);
+        const uint64_t l = cen_exp(q, mode);
+        Mont32 mo;
+        mo.init(p);
+        const uint32_t S = (uint32_t)(acc[e] % p);       // Montgomery form of the sum
+        if (l & 1) {
+            const uint64_t k2 = l + 1;                   // index 2k
+            const uint32_t N = cen_cnum(mo, 3, 4, 6, p - k2);
+            if (N == 0) {                                // C_k(3,4,6) == 0: another congruence
+                const unsigned long long f = atomicAdd(misc + 2, 1ull);
+                if (f < fix_cap) fix[f] = CenFix{i, e};
+                continue;
+            }
+            uint32_t r = mo.mul(S, mo.to(2 * k2));       // S (4k)
+            r = mo.mul(r, cen_pow(mo, mo.to(N), p - 2)); // / N
+            cen_emit(p, (uint32_t)k2, 1, mo.canon(r), e, res_out, pairs, pair_cap, misc);
+        } else {
+            const uint64_t k = (p - 1 - l) / 2;
+            uint32_t r = mo.mul(S, cen_pow(mo, mo.to(4), p - 2 * k));   // 4^{(p-1)-(2k-1)}
+            uint64_t v = mo.canon(r);
+            if ((k & 1) && v) v = p - v;
+            cen_emit(p, (uint32_t)l, 2, v, e, res_out, pairs, pair_cap, misc);
+        }
+    }
+}
+
+// fallback congruences for B_{2k} where C_k(3,4,6) == 0 (mod p): C_k(a,b,c) B_{2k} == sum of
+// S_{2k-1} over the intervals (VOR P:L245-249; (4,5,8) P:L263-268; eqnVandiver P:L171-175;
+// eqnTW1 b = 2, 4, 6, 7 P:L185-189)
+struct CenAlt { uint32_t a, b, c, min_p, n; uint32_t iv[3][4]; };
+__constant__ CenAlt c_cen_alt[7] = {
+    {2, 3, 4, 5, 1, {{1, 4, 1, 3}}},
+    {4, 5, 8, 7, 2, {{1, 8, 1, 5}, {3, 8, 2, 5}}},
+    {2, 5, 6, 7, 2, {{1, 6, 1, 5}, {1, 3, 2, 5}}},
+    {2, 2, 3, 5, 1, {{1, 3, 1, 2}}},
+    {2, 4, 5, 7, 2, {{1, 5, 1, 4}, {2, 5, 1, 2}}},
+    {2, 6, 7, 11, 3, {{1, 7, 1, 6}, {2, 7, 1, 3}, {3, 7, 1, 2}}},
+    {2, 7, 8, 11, 3, {{1, 8, 1, 7}, {2, 8, 2, 7}, {3, 8, 3, 7}}},
+};
+
+// one warp per queued entry: the first fallback with a unit C_k, its sums by per-term powers
+__global__ void census_fixup_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ ebase,
+                                    uint64_t i_lo, uint32_t mode, const CenFix *__restrict__ fix, uint64_t nfix,
+                                    uint64_t *__restrict__ res_out, CenPair *__restrict__ pairs, uint64_t pair_cap,
+                                    unsigned long long *__restrict__ misc) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t f = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; f < nfix; f += nwarps) {
+        const CenFix fx = fix[f];
+        const uint32_t p = (uint32_t)primes[fx.i];
+        const uint64_t q = fx.e - (ebase[fx.i] - ebase[i_lo]);
+        const uint64_t l = cen_exp(q, mode), k2 = l + 1;
+        Mont32 mo;
+        mo.init(p);
+        bool done = false;
+        // the table, then eqnTW1 for b = 8, 9, ... (p > b + 1): C_k(2,b,b+1) B_{2k} ==
+        // sum_{m=1}^{floor(b/2)} S_{2k-1}(m/(b+1), m/b).  All small-base numerators vanish together
+        // where a^{t-1} is a character of small order (e.g. t = (p+1)/2 with 2, 3, 5, 7 quadratic
+        // residues); a base b + 1 outside its kernel ends that (b <= 28 for every p < 30000).
+        for (uint32_t a = 0; a < 7 + CEN_TW_BMAX && !done; a++) {
+            uint32_t ca, cb, cc, n;
+            if (a < 7) {
+                const CenAlt &A = c_cen_alt[a];
+                if (p < A.min_p) continue;
+                ca = A.a; cb = A.b; cc = A.c; n = A.n;
+            } else {
+                const uint32_t b = a + 1;
+                if (p <= b + 1) break;
+                ca = 2; cb = b; cc = b + 1; n = b / 2;
+            }
+            const uint32_t N = cen_cnum(mo, ca, cb, cc, p - k2);
+            if (N == 0) continue;
+            uint32_t S = 0;
+            for (uint32_t t = 0; t < n; t++) {
+                uint32_t xn, xd, yn, yd;
+                if (a < 7) {
+                    xn = c_cen_alt[a].iv[t][0]; xd = c_cen_alt[a].iv[t][1];
+                    yn = c_cen_alt[a].iv[t][2]; yd = c_cen_alt[a].iv[t][3];
+                } else {
+                    xn = t + 1; xd = cc; yn = t + 1; yd = cb;        // (m/(b+1), m/b)
+                }
+                const uint64_t s_lo = (uint64_t)xn * p / xd + 1;                      // x p < s
+                const uint64_t yp = (uint64_t)yn * p;                                  // s < y p
+                const uint64_t s_hi = yp % yd ? yp / yd : yp / yd - 1;
+                for (uint64_t s = s_lo + lane; s <= s_hi; s += 32) S = mo.add(S, cen_pow(mo, mo.to(s), l));
+            }
+            #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) S = mo.add(S, __shfl_xor_sync(0xffffffffu, S, o));
+            uint32_t r = mo.mul(S, mo.to(2 * k2));
+            r = mo.mul(r, cen_pow(mo, mo.to(N), p - 2));
+            if (lane == 0) cen_emit(p, (uint32_t)k2, 1, mo.canon(r), fx.e, res_out, pairs, pair_cap, misc);
+            done = true;
+        }
+        if (!done && lane == 0) atomicAdd(misc + 3, 1ull);   // unresolved (reported as an error)
+    }
+}
+
+}  // namespace wv
