@@ -1095,7 +1095,7 @@ static int census_impl(uint64_t lo, uint64_t hi, uint32_t mode, wv_pair *out, si
     static_assert(sizeof(wv_pair) == sizeof(CenPair), "wv_pair layout");
     if (hi <= lo) return set_err(WV_EINVAL, "empty or inverted range [%llu, %llu)", (unsigned long long)lo,
                                  (unsigned long long)hi);
-    if (hi > CEN_HI_MAX) return set_err(WV_EINVAL, "census needs hi <= 2^30");
+    if (hi > CEN_HI_MAX) return set_err(WV_EINVAL, "census needs hi <= 2^26");
     if (mode < 1 || mode > 3) return set_err(WV_EINVAL, "mode %u not in {1,2,3}", mode);
     DevCtx *c;
     TRY(ctx_get(&c));

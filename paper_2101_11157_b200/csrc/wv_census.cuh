@@ -10,9 +10,10 @@
 // together over the multiplicative group: with g a primitive root and s_j = g^j,
 //     S_l(I) = sum_{0<=j<(p-1)/2} [s'_j in I] sigma_j (g^l)^j,   s'_j = min(s_j, p - s_j),
 // sigma_j = 1 if s'_j = s_j else (-1)^l (s_{j+(p-1)/2} = -s_j, so each pair {s, p-s} is visited
-// once).  One lane owns one exponent l: per step one Montgomery product w <- w g^l and a
-// predicated add; the membership code of s'_j is shared by the warp through shared memory.
-// Every index of a prime costs (p-1)/2 steps.
+// once).  One lane owns one exponent l; the membership codes of s'_j are shared by the warp, and
+// the sum over j is a polynomial in h = g^l with coefficients in {0, +1, -1}, evaluated by Horner
+// over blocks of 16 steps with table lookups inside a block (see census_walk_kernel).  Every index
+// of a prime costs (p-1)/2 steps.
 //
 // Where C_k(3,4,6) == 0 (mod p) the finalize kernel queues (p, l) for a fix-up that evaluates the
 // first congruence of a fixed list with a unit C_k directly (per-term powers; rare: ~1/p of the B
@@ -28,9 +29,9 @@ namespace wv {
 constexpr uint32_t CEN_SEG = 8192;             // walk steps per work item
 constexpr uint32_t CEN_TG = 4;                 // exponent tiles (of 32) per work item
 constexpr uint32_t CEN_TW_BMAX = 1024;         // fix-up: eqnTW1 parameters b <= this
-constexpr uint32_t CEN_THREADS = 256;
+constexpr uint32_t CEN_THREADS = 128;
 constexpr uint32_t CEN_WARPS = CEN_THREADS / 32;
-constexpr uint64_t CEN_HI_MAX = 1ull << 30;    // Mont32 lazy range
+constexpr uint64_t CEN_HI_MAX = 1ull << 26;    // lazy bounds of the Horner walk
 
 // Montgomery power: b in Montgomery form, result in Montgomery form ([0, 2p))
 __device__ __forceinline__ uint32_t cen_pow(const Mont32 &mo, uint32_t b, uint64_t e) {
@@ -79,34 +80,40 @@ __global__ void census_plan_kernel(const uint64_t *__restrict__ primes, uint64_t
         }
         groot[i] = g;
         const uint64_t ne = cen_nexp(p, mode);
-        const uint64_t half = (p - 1) / 2;
+        const uint64_t half = (p - 1) / 2, tiles = (mode == 3 ? 2 : 1) * (((p - 3) / 2 + 31) / 32);
         nexp[i] = ne;
-        nitems[i] = ((ne + 32 * CEN_TG - 1) / (32 * CEN_TG)) * ((half + CEN_SEG - 1) / CEN_SEG);
+        nitems[i] = ((tiles + CEN_TG - 1) / CEN_TG) * ((half + CEN_SEG - 1) / CEN_SEG);
     }
 }
 
-// membership code of s' = min(s, p - s) for one walk step:
-//   bit 0: s' in (p/6, p/4) and s' = s      (B, sigma = +1)
-//   bit 1: s' in (p/6, p/4) and s' = p - s  (B, sigma = (-1)^l = -1 for odd l)
-//   bit 2: s' in (0, p/4)                   (E, sigma = +1 for even l)
-__device__ __forceinline__ uint32_t cen_code(uint32_t s, uint32_t p) {
-    const uint32_t sp = s <= p - s ? s : p - s;
-    const bool neg = sp != s;
-    const bool q4 = 4ull * sp < p;
-    const bool inb = q4 && 6ull * sp > p;
-    return (inb ? (neg ? 2u : 1u) : 0u) | (q4 ? 4u : 0u);
+// Persistent walk.  Items: (prime i, group of CEN_TG exponent tiles, walk segment of CEN_SEG
+// steps).  A tile is 32 exponents of one parity (B: odd l, E: even l), one per lane, so the
+// membership codes are warp-uniform.  Per segment the warp writes three bit masks (B with
+// sigma = +1, B with sigma = -1, E) of its steps j; per tile each lane evaluates
+//     sum_j c_j h^j  (h = g^l, c_j in {0, +1, -1})
+// by Horner over blocks of 16 steps from the last block down:  acc <- acc h^16 + inner_J, with
+// inner_J = sum_{d<16} c_{16J+d} h^d read from per-lane subset-sum tables of {h^{4n+b}: b < 4}
+// (4 nibbles x 16 entries, shared memory, uniform index) -- 4 (E) or 8 (B) table reads and one
+// Montgomery step per 16 walk steps.  Lazy bounds (p < 2^26): table entries < 4p, inner < 32p,
+// acc < 40p, REDC(acc H + inner R) < 40p.
+constexpr uint32_t CEN_WORDS = CEN_SEG / 32;
+
+__device__ __forceinline__ uint32_t cen_horner(const Mont32 &mo, uint32_t acc, uint32_t H, uint32_t in) {
+    const uint64_t T = (uint64_t)acc * H + ((uint64_t)in << 32);
+    const uint32_t m = (uint32_t)T * mo.pinv;
+    return (uint32_t)((T + (uint64_t)m * mo.p) >> 32);
 }
 
-// Persistent walk: each warp takes items (prime i, tile group, walk segment); lane = exponent.
-// acc[ebase[i] - ebase[i_lo] + q] += the segment's sum (canonical Montgomery form, < p per item).
 __global__ void __launch_bounds__(CEN_THREADS)
 census_walk_kernel(const uint64_t *__restrict__ primes, const uint32_t *__restrict__ groot,
                    const uint64_t *__restrict__ istart, const uint64_t *__restrict__ ebase, uint64_t i_lo,
-                   uint64_t i_hi, uint32_t mode, unsigned long long *__restrict__ acc,
+                   uint64_t i_hi, uint32_t mode, unsigned long long *__restrict__ acc_out,
                    unsigned long long *__restrict__ counter) {
-    __shared__ uint32_t s_code[CEN_WARPS][CEN_SEG / 8];     // 4-bit codes, 8 per word
+    __shared__ uint32_t s_bp[CEN_WARPS][CEN_WORDS], s_bn[CEN_WARPS][CEN_WORDS], s_e[CEN_WARPS][CEN_WORDS];
+    __shared__ uint32_t s_tab[CEN_WARPS][4][16][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t g_lo = istart[i_lo], g_hi = istart[i_hi];
+    uint32_t (*tab)[16][32] = s_tab[wid];
     for (;;) {
         unsigned long long gi = 0;
         if (lane == 0) gi = atomicAdd(counter, 1ull);
@@ -118,65 +125,98 @@ census_walk_kernel(const uint64_t *__restrict__ primes, const uint32_t *__restri
         const uint64_t c = g - istart[i];
         const uint32_t half = (p - 1) / 2;
         const uint32_t nseg = (half + CEN_SEG - 1) / CEN_SEG;
-        const uint64_t tg = c / nseg;
+        const uint64_t grp = c / nseg;
         const uint32_t seg = (uint32_t)(c % nseg);
         const uint32_t j0 = seg * CEN_SEG;
         const uint32_t len = half - j0 < CEN_SEG ? half - j0 : CEN_SEG;
         Mont32 mo;
         mo.init(p);
         const uint32_t gm = mo.to(groot[i]);
-        // codes of s_j = g^j, j in [j0, j0 + len): lane writes words wd = lane, lane + 32, ...
-        // (8 codes each).  s is kept plain: mul(s, g R) = s g (mod p).
-        const uint32_t nw = (len + 7) / 8;
+        // codes of s_j = g^{j0 + j}, j < len (s kept plain: mul(s, g R) = s g mod p)
+        const uint32_t nwords = (len + 31) / 32;
         {
-            const uint32_t g256 = cen_pow(mo, gm, 256);
-            uint32_t s0 = (uint32_t)mo.canon(cen_pow(mo, gm, (uint64_t)j0 + 8 * lane));
-            for (uint32_t wd = lane; wd < nw; wd += 32) {
-                uint32_t s = s0, word = 0;
-                #pragma unroll
-                for (int b = 0; b < 8; b++) {
-                    if (8 * wd + b < len) word |= cen_code(s, p) << (4 * b);
+            const uint32_t g1024 = cen_pow(mo, gm, 1024);
+            uint32_t s0 = (uint32_t)mo.canon(cen_pow(mo, gm, (uint64_t)j0 + 32 * lane));
+            for (uint32_t wd = lane; wd < nwords; wd += 32) {
+                uint32_t s = s0, bp = 0, bn = 0, be = 0;
+                #pragma unroll 8
+                for (uint32_t b = 0; b < 32; b++) {
+                    if (32 * wd + b < len) {
+                        const uint32_t sp = s <= p - s ? s : p - s;
+                        const bool q4 = 4ull * sp < p, inb = q4 && 6ull * sp > p;
+                        bp |= (uint32_t)(inb && sp == s) << b;
+                        bn |= (uint32_t)(inb && sp != s) << b;
+                        be |= (uint32_t)q4 << b;
+                    }
                     s = mo.mul(s, gm);
                     s = s >= p ? s - p : s;
                 }
-                s_code[wid][wd] = word;
-                s0 = mo.mul(s0, g256);
+                s_bp[wid][wd] = bp;
+                s_bn[wid][wd] = bn;
+                s_e[wid][wd] = be;
+                s0 = mo.mul(s0, g1024);
                 s0 = s0 >= p ? s0 - p : s0;
             }
         }
         __syncwarp();
-        const uint64_t ne = cen_nexp(p, mode);
+        const uint64_t nhalf = (p - 3) / 2;                 // exponents per parity
+        const uint64_t tB = mode == 2 ? 0 : (nhalf + 31) / 32, tE = mode == 1 ? 0 : (nhalf + 31) / 32;
+        const uint32_t nblk = (len + 15) / 16;
         for (uint32_t tt = 0; tt < CEN_TG; tt++) {
-            const uint64_t q = (tg * CEN_TG + tt) * 32 + lane;
-            if ((tg * CEN_TG + tt) * 32 >= ne) break;                 // warp-uniform
-            const bool valid = q < ne;
-            const uint64_t l = cen_exp(valid ? q : 0, mode);
-            const uint32_t h = cen_pow(mo, gm, l);                   // g^l
-            uint32_t w = cen_pow(mo, h, j0);                         // g^{l j0}
-            const uint32_t sh = (l & 1) ? 0u : 2u;                   // odd l: bits 0/1; even l: bit 2
-            uint32_t a = 0;                                          // lazy sum in [0, 2p)
-            for (uint32_t wd = 0; wd < nw; wd++) {
-                const uint32_t word = s_code[wid][wd] >> sh;
-                if (8 * wd + 8 <= len) {
-                    #pragma unroll
-                    for (uint32_t b = 0; b < 8; b++) {
-                        const uint32_t t = (word >> (4 * b)) & 3u;  // 0: none, 1: +w, 2: -w
-                        const uint32_t v = t == 0 ? 0u : (t == 1 ? w : mo.p2 - w);
-                        a = mo.add(a, v);
-                        w = mo.mul(w, h);
-                    }
-                } else {
-                    for (uint32_t b = 0; 8 * wd + b < len; b++) {
-                        const uint32_t t = (word >> (4 * b)) & 3u;
-                        const uint32_t v = t == 0 ? 0u : (t == 1 ? w : mo.p2 - w);
-                        a = mo.add(a, v);
-                        w = mo.mul(w, h);
-                    }
+            const uint64_t t = grp * CEN_TG + tt;
+            if (t >= tB + tE) break;                         // warp-uniform
+            const bool isB = t < tB;
+            const uint64_t u = (isB ? t : t - tB) * 32 + lane;
+            const bool valid = u < nhalf;
+            const uint64_t l = isB ? 2 * u + 1 : 2 * u + 2;
+            const uint64_t q = mode == 3 ? l - 1 : u;
+            const uint32_t h = cen_pow(mo, gm, valid ? l : 1);
+            // h^d, d < 16 (canonical Montgomery form), subset-sum tables, H = h^16
+            uint32_t hp[16];
+            hp[0] = mo.r1;
+            #pragma unroll
+            for (int d = 1; d < 16; d++) {
+                const uint32_t x = mo.mul(hp[d - 1], h);
+                hp[d] = x >= p ? x - p : x;
+            }
+            uint32_t H = mo.mul(hp[15], h);
+            H = H >= p ? H - p : H;
+            __syncwarp();
+            #pragma unroll
+            for (int n = 0; n < 4; n++) {
+                uint32_t v[16];
+                v[0] = 0;
+                #pragma unroll
+                for (int x = 1; x < 16; x++) v[x] = v[x & (x - 1)] + hp[4 * n + ((x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : 3)];
+                #pragma unroll
+                for (int x = 0; x < 16; x++) tab[n][x][lane] = v[x];
+            }
+            __syncwarp();
+            uint32_t acc = 0;
+            const uint32_t p16 = 16 * p;
+            if (isB) {
+                for (int J = (int)nblk - 1; J >= 0; J--) {
+                    const uint32_t sh = (J & 1) * 16;
+                    const uint32_t bp = (s_bp[wid][J >> 1] >> sh) & 0xffffu, bn = (s_bn[wid][J >> 1] >> sh) & 0xffffu;
+                    const uint32_t pos = tab[0][bp & 15][lane] + tab[1][(bp >> 4) & 15][lane] +
+                                         tab[2][(bp >> 8) & 15][lane] + tab[3][bp >> 12][lane];
+                    const uint32_t neg = tab[0][bn & 15][lane] + tab[1][(bn >> 4) & 15][lane] +
+                                         tab[2][(bn >> 8) & 15][lane] + tab[3][bn >> 12][lane];
+                    acc = cen_horner(mo, acc, H, pos + p16 - neg);
+                }
+            } else {
+                for (int J = (int)nblk - 1; J >= 0; J--) {
+                    const uint32_t be = (s_e[wid][J >> 1] >> ((J & 1) * 16)) & 0xffffu;
+                    const uint32_t pos = tab[0][be & 15][lane] + tab[1][(be >> 4) & 15][lane] +
+                                         tab[2][(be >> 8) & 15][lane] + tab[3][be >> 12][lane];
+                    acc = cen_horner(mo, acc, H, pos);
                 }
             }
             if (valid) {
-                const uint32_t r = a >= p ? a - p : a;
-                atomicAdd(acc + (ebase[i] - ebase[i_lo]) + q, (unsigned long long)r);
+                // times h^{j0} (segment offset), canonical
+                const uint32_t w0 = cen_pow(mo, h, j0);
+                const uint32_t r = (uint32_t)(((uint64_t)mo.mul(acc, w0)) % p);
+                atomicAdd(acc_out + (ebase[i] - ebase[i_lo]) + q, (unsigned long long)r);
             }
         }
         __syncwarp();

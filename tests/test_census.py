@@ -190,6 +190,6 @@ def test_census_edges(wv):
     assert len(wv.census_residues(24, 29, wv.MODE_BOTH)) == 0
     p, n, c = wv.census(24, 29, wv.MODE_BOTH)
     assert len(p) == 0 and n == 0 and c == 0
-    for args in ((10, 10, 3), (10, 5, 3), (5, 100, 0), (5, 100, 4), (5, (1 << 30) + 1, 3)):
+    for args in ((10, 10, 3), (10, 5, 3), (5, 100, 0), (5, 100, 4), (5, (1 << 26) + 1, 3)):
         with pytest.raises(wv.WVError):
             wv.census(*args)
