@@ -1167,8 +1167,8 @@ static int census_impl(uint64_t lo, uint64_t hi, uint32_t mode, wv_pair *out, si
             CK(cudaMemsetAsync(d_misc + 2, 0, 24, st));  // fix count, unresolved, walk counter
             LAUNCH(census_walk_kernel, c->sms * c->occ_census, CEN_THREADS, st, d_primes, d_g, d_is, d_eb, i0, i1,
                    mode, d_acc, d_misc + 4);
-            const unsigned gf = (unsigned)((nE + 255) / 256 < (uint64_t)c->sms * 16 ? (nE + 255) / 256 : c->sms * 16);
-            LAUNCH(census_finalize_kernel, gf, 256, st, d_primes, d_eb, i0, i1, mode, d_acc, d_res, d_pairs, pcap,
+            const unsigned gf = (unsigned)((i1 - i0) < (uint64_t)c->sms * 8 ? (i1 - i0) : c->sms * 8);
+            LAUNCH(census_finalize_kernel, gf, CEN_FIN_T, st, d_primes, d_eb, i0, i1, mode, d_acc, d_res, d_pairs, pcap,
                    d_fix, fcap, d_misc);
             uint64_t hm[2] = {0, 0};
             CK(cudaMemcpyAsync(hm, d_misc + 2, 16, cudaMemcpyDeviceToHost, st));

@@ -231,16 +231,22 @@ __host__ __device__ __forceinline__ uint64_t cen_checksum_term(uint64_t p, uint3
     return mix64(p ^ ((uint64_t)index << 32) ^ rotl64(res, 17) ^ ((uint64_t)kind << 62));
 }
 
-// outputs of one index residue: residue array, zero -> pair list, checksum
+// outputs of one index residue: residue array, zero -> pair list; the checksum term is added to
+// the caller's register sum (flushed once per warp by cen_flush: one global atomic per warp)
 __device__ __forceinline__ void cen_emit(uint64_t p, uint32_t index, uint32_t kind, uint64_t res, uint64_t e,
                                          uint64_t *__restrict__ res_out, CenPair *__restrict__ pairs,
-                                         uint64_t pair_cap, unsigned long long *__restrict__ misc) {
+                                         uint64_t pair_cap, unsigned long long *__restrict__ misc, uint64_t &chk) {
     if (res_out) res_out[e] = res;
     if (res == 0) {
         const unsigned long long k = atomicAdd(misc + 0, 1ull);
         if (k < pair_cap) pairs[k] = CenPair{p, index, kind};
     }
-    atomicAdd(misc + 1, (unsigned long long)cen_checksum_term(p, index, kind, res));
+    chk += cen_checksum_term(p, index, kind, res);
+}
+__device__ __forceinline__ void cen_flush(uint64_t chk, unsigned long long *__restrict__ misc) {
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) chk += __shfl_xor_sync(0xffffffffu, chk, o);
+    if ((threadIdx.x & 31) == 0 && chk) atomicAdd(misc + 1, (unsigned long long)chk);
 }
 
 // C_k(3,4,6) numerator 3^t + 4^t - 6^t - 1 (t = p - 2k), canonical
@@ -252,47 +258,113 @@ __device__ __forceinline__ uint32_t cen_cnum(const Mont32 &mo, uint32_t a, uint3
     return (uint32_t)mo.canon(x);
 }
 
-// one thread per batch entry e: residue from the walked sum
-//   odd l = 2k-1:  B_{2k} = S (4k) / (3^t + 4^t - 6^t - 1),  t = p - 2k     (eqnSV)
-//   even l = t:    E_t = (-1)^k 4^{-(2k-1)} S,  2k = p - 1 - t              (eqnE1, reading R10)
-__global__ void census_finalize_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ ebase,
-                                       uint64_t i_lo, uint64_t i_hi, uint32_t mode,
-                                       const unsigned long long *__restrict__ acc, uint64_t *__restrict__ res_out,
-                                       CenPair *__restrict__ pairs, uint64_t pair_cap, CenFix *__restrict__ fix,
-                                       uint64_t fix_cap, unsigned long long *__restrict__ misc) {
-    const uint64_t nE = ebase[i_hi] - ebase[i_lo];
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nE; e += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t lo = i_lo, hi = i_hi;                 // ebase[lo] - ebase[i_lo] <= e < ebase[hi] - ...
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) / 2;
-            if (ebase[mid] - ebase[i_lo] <= e) lo = mid; else hi = mid;
-        }
-        const uint64_t i = lo;
+// One block per prime (grid-stride over the batch's primes), thread tid takes positions
+// q = tid, tid + CEN_FIN_T, ... of that prime, so its exponents l advance by a fixed step dl:
+//   odd l = 2k-1:  B_{2k} = S (4k) / N,  N = 3^t + 4^t - 6^t - 1,  t = p - 2k     (eqnSV)
+//   even l:        E_l = (-1)^k 4^{p-2k} S,  2k = p - 1 - l                       (eqnE1, R10)
+// The powers 3^t, 4^t, 6^t (t falls by dl) and 4^{p-2k} (rises by dl) are advanced by one product
+// each; the B inverses are batched 8 at a time per thread (one Fermat inverse per batch).
+constexpr uint32_t CEN_FIN_T = 256;
+constexpr int CEN_FIN_BATCH = 8;
+
+__global__ void __launch_bounds__(CEN_FIN_T)
+census_finalize_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ ebase,
+                       uint64_t i_lo, uint64_t i_hi, uint32_t mode, const unsigned long long *__restrict__ acc,
+                       uint64_t *__restrict__ res_out, CenPair *__restrict__ pairs, uint64_t pair_cap,
+                       CenFix *__restrict__ fix, uint64_t fix_cap, unsigned long long *__restrict__ misc) {
+    const uint32_t tid = threadIdx.x;
+    uint64_t chk = 0;
+    for (uint64_t i = i_lo + blockIdx.x; i < i_hi; i += gridDim.x) {
         const uint32_t p = (uint32_t)primes[i];
-        const uint64_t q = e - (ebase[i] - ebase[i_lo]);
-        const uint64_t l = cen_exp(q, mode);
+        const uint64_t base = ebase[i] - ebase[i_lo], ne = ebase[i + 1] - ebase[i];
+        if (tid >= ne) continue;
         Mont32 mo;
         mo.init(p);
-        const uint32_t S = (uint32_t)(acc[e] % p);       // Montgomery form of the sum
-        if (l & 1) {
-            const uint64_t k2 = l + 1;                   // index 2k
-            const uint32_t N = cen_cnum(mo, 3, 4, 6, p - k2);
-            if (N == 0) {                                // C_k(3,4,6) == 0: another congruence
-                const unsigned long long f = atomicAdd(misc + 2, 1ull);
-                if (f < fix_cap) fix[f] = CenFix{i, e};
-                continue;
+        const uint64_t l0 = cen_exp(tid, mode);
+        const uint64_t dl = (mode == 3 ? 1 : 2) * (uint64_t)CEN_FIN_T;      // exponent step per iteration
+        const uint64_t dlm = dl % (p - 1);
+        if (l0 & 1) {                                    // B entries (odd l)
+            const uint64_t t0 = p - (l0 + 1);           // t = p - 2k, falls by dl
+            const uint64_t back = (p - 1) - dlm;         // x^{-dl} = x^{(p-1) - dl mod (p-1)}
+            const uint32_t m3 = mo.to(3), m4 = mo.to(4), m6 = mo.to(6);
+            uint32_t p3 = cen_pow(mo, m3, t0), p4 = cen_pow(mo, m4, t0), p6 = cen_pow(mo, m6, t0);
+            const uint32_t s3 = cen_pow(mo, m3, back), s4 = cen_pow(mo, m4, back), s6 = cen_pow(mo, m6, back);
+            uint32_t pend_x[CEN_FIN_BATCH], pend_n[CEN_FIN_BATCH];  // S (4k) and N (Montgomery form)
+            uint64_t pend_q[CEN_FIN_BATCH];
+            int np = 0;
+            for (uint64_t q = tid; q < ne; q += CEN_FIN_T) {
+                const uint64_t l = cen_exp(q, mode), k2 = l + 1;
+                uint32_t N = mo.add(p3, p4);
+                N = mo.add(N, mo.p2 - p6);
+                N = mo.add(N, mo.p2 - mo.r1);
+                p3 = mo.mul(p3, s3); p4 = mo.mul(p4, s4); p6 = mo.mul(p6, s6);
+                const uint32_t Sm = (uint32_t)(acc[base + q] % p);
+                if (mo.canon(N) == 0) {                  // C_k(3,4,6) == 0: another congruence
+                    const unsigned long long f = atomicAdd(misc + 2, 1ull);
+                    if (f < fix_cap) fix[f] = CenFix{i, base + q};
+                    continue;
+                }
+                pend_x[np] = mo.mul(Sm, mo.to(2 * k2));
+                pend_n[np] = N;
+                pend_q[np] = q;
+                np++;
+                const bool last = q + CEN_FIN_T >= ne;
+                if (np == CEN_FIN_BATCH || last) {
+                    // Montgomery's trick: one inverse for the batch
+                    uint32_t pre[CEN_FIN_BATCH];
+                    uint32_t run = mo.r1;
+                    #pragma unroll
+                    for (int u = 0; u < CEN_FIN_BATCH; u++) {
+                        if (u < np) { pre[u] = run; run = mo.mul(run, pend_n[u]); }
+                    }
+                    uint32_t inv = cen_pow(mo, run, p - 2);
+                    #pragma unroll
+                    for (int u = CEN_FIN_BATCH - 1; u >= 0; u--) {
+                        if (u < np) {
+                            const uint32_t iu = mo.mul(inv, pre[u]);         // 1 / N_u
+                            inv = mo.mul(inv, pend_n[u]);
+                            const uint64_t lq = cen_exp(pend_q[u], mode);
+                            cen_emit(p, (uint32_t)(lq + 1), 1, mo.canon(mo.mul(pend_x[u], iu)), base + pend_q[u],
+                                     res_out, pairs, pair_cap, misc, chk);
+                        }
+                    }
+                    np = 0;
+                }
             }
-            uint32_t r = mo.mul(S, mo.to(2 * k2));       // S (4k)
-            r = mo.mul(r, cen_pow(mo, mo.to(N), p - 2)); // / N
-            cen_emit(p, (uint32_t)k2, 1, mo.canon(r), e, res_out, pairs, pair_cap, misc);
-        } else {
-            const uint64_t k = (p - 1 - l) / 2;
-            uint32_t r = mo.mul(S, cen_pow(mo, mo.to(4), p - 2 * k));   // 4^{(p-1)-(2k-1)}
-            uint64_t v = mo.canon(r);
-            if ((k & 1) && v) v = p - v;
-            cen_emit(p, (uint32_t)l, 2, v, e, res_out, pairs, pair_cap, misc);
+            if (np) {                                    // (only when the last entries were fix-ups)
+                uint32_t pre[CEN_FIN_BATCH];
+                uint32_t run = mo.r1;
+                #pragma unroll
+                for (int u = 0; u < CEN_FIN_BATCH; u++) {
+                    if (u < np) { pre[u] = run; run = mo.mul(run, pend_n[u]); }
+                }
+                uint32_t inv = cen_pow(mo, run, p - 2);
+                #pragma unroll
+                for (int u = CEN_FIN_BATCH - 1; u >= 0; u--) {
+                    if (u < np) {
+                        const uint32_t iu = mo.mul(inv, pre[u]);
+                        inv = mo.mul(inv, pend_n[u]);
+                        const uint64_t lq = cen_exp(pend_q[u], mode);
+                        cen_emit(p, (uint32_t)(lq + 1), 1, mo.canon(mo.mul(pend_x[u], iu)), base + pend_q[u],
+                                 res_out, pairs, pair_cap, misc, chk);
+                    }
+                }
+            }
+        } else {                                         // E entries (even l): 4^{p-2k} = 4^{l+1}
+            const uint32_t m4 = mo.to(4);
+            uint32_t f = cen_pow(mo, m4, l0 + 1);
+            const uint32_t sf = cen_pow(mo, m4, dlm);
+            for (uint64_t q = tid; q < ne; q += CEN_FIN_T) {
+                const uint64_t l = cen_exp(q, mode), k = (p - 1 - l) / 2;
+                const uint32_t Sm = (uint32_t)(acc[base + q] % p);
+                uint64_t v = mo.canon(mo.mul(Sm, f));
+                f = mo.mul(f, sf);
+                if ((k & 1) && v) v = p - v;
+                cen_emit(p, (uint32_t)l, 2, v, base + q, res_out, pairs, pair_cap, misc, chk);
+            }
         }
     }
+    cen_flush(chk, misc);
 }
 
 // fallback congruences for B_{2k} where C_k(3,4,6) == 0 (mod p): C_k(a,b,c) B_{2k} == sum of
@@ -315,6 +387,7 @@ __global__ void census_fixup_kernel(const uint64_t *__restrict__ primes, const u
                                     uint64_t *__restrict__ res_out, CenPair *__restrict__ pairs, uint64_t pair_cap,
                                     unsigned long long *__restrict__ misc) {
     const int lane = threadIdx.x & 31;
+    uint64_t chk = 0;
     const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
     for (uint64_t f = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; f < nfix; f += nwarps) {
         const CenFix fx = fix[f];
@@ -359,11 +432,12 @@ __global__ void census_fixup_kernel(const uint64_t *__restrict__ primes, const u
             for (int o = 16; o > 0; o >>= 1) S = mo.add(S, __shfl_xor_sync(0xffffffffu, S, o));
             uint32_t r = mo.mul(S, mo.to(2 * k2));
             r = mo.mul(r, cen_pow(mo, mo.to(N), p - 2));
-            if (lane == 0) cen_emit(p, (uint32_t)k2, 1, mo.canon(r), fx.e, res_out, pairs, pair_cap, misc);
+            if (lane == 0) cen_emit(p, (uint32_t)k2, 1, mo.canon(r), fx.e, res_out, pairs, pair_cap, misc, chk);
             done = true;
         }
         if (!done && lane == 0) atomicAdd(misc + 3, 1ull);   // unresolved (reported as an error)
     }
+    cen_flush(chk, misc);
 }
 
 }  // namespace wv
