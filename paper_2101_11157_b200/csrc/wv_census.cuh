@@ -26,8 +26,8 @@
 
 namespace wv {
 
-constexpr uint32_t CEN_SEG = 8192;             // walk steps per work item
-constexpr uint32_t CEN_TG = 4;                 // exponent tiles (of 32) per work item
+constexpr uint32_t CEN_SEG = 4096;             // walk steps per work item
+constexpr uint32_t CEN_TG = 8;                 // exponent tiles (of 32) per work item
 constexpr uint32_t CEN_TW_BMAX = 1024;         // fix-up: eqnTW1 parameters b <= this
 constexpr uint32_t CEN_THREADS = 128;
 constexpr uint32_t CEN_WARPS = CEN_THREADS / 32;
@@ -98,10 +98,25 @@ __global__ void census_plan_kernel(const uint64_t *__restrict__ primes, uint64_t
 // acc < 40p, REDC(acc H + inner R) < 40p.
 constexpr uint32_t CEN_WORDS = CEN_SEG / 32;
 
+__device__ __forceinline__ uint32_t cen_lds(uint32_t addr) {     // 32-bit shared load, shared address
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t cen_horner(const Mont32 &mo, uint32_t acc, uint32_t H, uint32_t in) {
-    const uint64_t T = (uint64_t)acc * H + ((uint64_t)in << 32);
-    const uint32_t m = (uint32_t)T * mo.pinv;
-    return (uint32_t)((T + (uint64_t)m * mo.p) >> 32);
+    // REDC(acc H + in 2^32): T = acc H + (in << 32); m = T_lo pinv; (T + m p) >> 32 -- three IMADs
+    uint32_t r;
+    asm("{\n\t.reg .u64 t, z;\n\t.reg .u32 lo, m, hi;\n\t"
+        "mov.b64 z, {0, %4};\n\t"
+        "mad.wide.u32 t, %1, %2, z;\n\t"
+        "cvt.u32.u64 lo, t;\n\t"
+        "mul.lo.u32 m, lo, %3;\n\t"
+        "mad.wide.u32 t, m, %5, t;\n\t"
+        "mov.b64 {lo, hi}, t;\n\t"
+        "mov.u32 %0, hi;\n\t}"
+        : "=r"(r) : "r"(acc), "r"(H), "r"(mo.pinv), "r"(in), "r"(mo.p));
+    return r;
 }
 
 __global__ void __launch_bounds__(CEN_THREADS)
@@ -110,10 +125,17 @@ census_walk_kernel(const uint64_t *__restrict__ primes, const uint32_t *__restri
                    uint64_t i_hi, uint32_t mode, unsigned long long *__restrict__ acc_out,
                    unsigned long long *__restrict__ counter) {
     __shared__ uint32_t s_bp[CEN_WARPS][CEN_WORDS], s_bn[CEN_WARPS][CEN_WORDS], s_e[CEN_WARPS][CEN_WORDS];
-    __shared__ uint32_t s_tab[CEN_WARPS][4][16][32];
+    // per-warp tables [4][16][32] (8 KB), placed at an 8 KB-aligned shared address at run time so a
+    // table address is  base | (nibble << 7) | (n << 11)  -- one LOP3, no add (the static
+    // attribute alone does not fix the absolute shared address)
+    __shared__ uint32_t s_tabraw[CEN_WARPS * 2048 + 2048];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t g_lo = istart[i_lo], g_hi = istart[i_hi];
-    uint32_t (*tab)[16][32] = s_tab[wid];
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(s_tabraw);
+    const uint32_t al = (raw + 8191u) & ~8191u;
+    uint32_t *tabw = s_tabraw + (al - raw) / 4 + wid * 2048;          // [n][x][lane] = tabw[(16 n + x) 32 + lane]
+    const uint32_t tb = al + wid * 8192u + lane * 4u;
+    const uint32_t t0 = tb, t1 = tb | 0x800u, t2 = tb | 0x1000u, t3 = tb | 0x1800u;
     for (;;) {
         unsigned long long gi = 0;
         if (lane == 0) gi = atomicAdd(counter, 1ull);
@@ -189,27 +211,54 @@ census_walk_kernel(const uint64_t *__restrict__ primes, const uint32_t *__restri
                 #pragma unroll
                 for (int x = 1; x < 16; x++) v[x] = v[x & (x - 1)] + hp[4 * n + ((x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : 3)];
                 #pragma unroll
-                for (int x = 0; x < 16; x++) tab[n][x][lane] = v[x];
+                for (int x = 0; x < 16; x++) tabw[(16 * n + x) * 32 + lane] = v[x];
             }
             __syncwarp();
             uint32_t acc = 0;
             const uint32_t p16 = 16 * p;
+            // blocks J = nblk-1 .. 0, two per code word (block 2w: low half, 2w+1: high half)
             if (isB) {
-                for (int J = (int)nblk - 1; J >= 0; J--) {
-                    const uint32_t sh = (J & 1) * 16;
-                    const uint32_t bp = (s_bp[wid][J >> 1] >> sh) & 0xffffu, bn = (s_bn[wid][J >> 1] >> sh) & 0xffffu;
-                    const uint32_t pos = tab[0][bp & 15][lane] + tab[1][(bp >> 4) & 15][lane] +
-                                         tab[2][(bp >> 8) & 15][lane] + tab[3][bp >> 12][lane];
-                    const uint32_t neg = tab[0][bn & 15][lane] + tab[1][(bn >> 4) & 15][lane] +
-                                         tab[2][(bn >> 8) & 15][lane] + tab[3][bn >> 12][lane];
-                    acc = cen_horner(mo, acc, H, pos + p16 - neg);
+                int J = (int)nblk - 1;
+                if (!(J & 1)) {                                  // odd count: the lone top block first
+                    const uint32_t bp = s_bp[wid][J >> 1], bn = s_bn[wid][J >> 1];
+                    acc = cen_horner(mo, acc, H, cen_lds(t0 | ((bp << 7) & 0x780u)) + cen_lds(t1 | ((bp << 3) & 0x780u)) +
+                                                 cen_lds(t2 | ((bp >> 1) & 0x780u)) + cen_lds(t3 | ((bp >> 5) & 0x780u)) +
+                                                 p16 - (cen_lds(t0 | ((bn << 7) & 0x780u)) + cen_lds(t1 | ((bn << 3) & 0x780u)) +
+                                                        cen_lds(t2 | ((bn >> 1) & 0x780u)) + cen_lds(t3 | ((bn >> 5) & 0x780u))));
+                    J--;
+                }
+                for (; J > 0; J -= 2) {
+                    const uint32_t wp = s_bp[wid][J >> 1], wn = s_bn[wid][J >> 1];
+                    {
+                        const uint32_t bp = wp >> 16, bn = wn >> 16;
+                        acc = cen_horner(mo, acc, H, cen_lds(t0 | ((bp << 7) & 0x780u)) + cen_lds(t1 | ((bp << 3) & 0x780u)) +
+                                                     cen_lds(t2 | ((bp >> 1) & 0x780u)) + cen_lds(t3 | ((bp >> 5) & 0x780u)) +
+                                                     p16 - (cen_lds(t0 | ((bn << 7) & 0x780u)) + cen_lds(t1 | ((bn << 3) & 0x780u)) +
+                                                            cen_lds(t2 | ((bn >> 1) & 0x780u)) + cen_lds(t3 | ((bn >> 5) & 0x780u))));
+                    }
+                    {
+                        const uint32_t bp = wp, bn = wn;
+                        acc = cen_horner(mo, acc, H, cen_lds(t0 | ((bp << 7) & 0x780u)) + cen_lds(t1 | ((bp << 3) & 0x780u)) +
+                                                     cen_lds(t2 | ((bp >> 1) & 0x780u)) + cen_lds(t3 | ((bp >> 5) & 0x780u)) +
+                                                     p16 - (cen_lds(t0 | ((bn << 7) & 0x780u)) + cen_lds(t1 | ((bn << 3) & 0x780u)) +
+                                                            cen_lds(t2 | ((bn >> 1) & 0x780u)) + cen_lds(t3 | ((bn >> 5) & 0x780u))));
+                    }
                 }
             } else {
-                for (int J = (int)nblk - 1; J >= 0; J--) {
-                    const uint32_t be = (s_e[wid][J >> 1] >> ((J & 1) * 16)) & 0xffffu;
-                    const uint32_t pos = tab[0][be & 15][lane] + tab[1][(be >> 4) & 15][lane] +
-                                         tab[2][(be >> 8) & 15][lane] + tab[3][be >> 12][lane];
-                    acc = cen_horner(mo, acc, H, pos);
+                int J = (int)nblk - 1;
+                if (!(J & 1)) {
+                    const uint32_t be = s_e[wid][J >> 1];
+                    acc = cen_horner(mo, acc, H, cen_lds(t0 | ((be << 7) & 0x780u)) + cen_lds(t1 | ((be << 3) & 0x780u)) +
+                                                 cen_lds(t2 | ((be >> 1) & 0x780u)) + cen_lds(t3 | ((be >> 5) & 0x780u)));
+                    J--;
+                }
+                for (; J > 0; J -= 2) {
+                    const uint32_t we = s_e[wid][J >> 1];
+                    const uint32_t bh = we >> 16;
+                    acc = cen_horner(mo, acc, H, cen_lds(t0 | ((bh << 7) & 0x780u)) + cen_lds(t1 | ((bh << 3) & 0x780u)) +
+                                                 cen_lds(t2 | ((bh >> 1) & 0x780u)) + cen_lds(t3 | ((bh >> 5) & 0x780u)));
+                    acc = cen_horner(mo, acc, H, cen_lds(t0 | ((we << 7) & 0x780u)) + cen_lds(t1 | ((we << 3) & 0x780u)) +
+                                                 cen_lds(t2 | ((we >> 1) & 0x780u)) + cen_lds(t3 | ((we >> 5) & 0x780u)));
                 }
             }
             if (valid) {
