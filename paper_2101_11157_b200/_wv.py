@@ -246,12 +246,16 @@ def near_misses_device(primes, res_w, res_v, n, bound=50, histograms=True, cap=1
         (hv.cpu().numpy().view(np.uint64) if hv is not None else z)
 
 
-def residues_device(primes, mode=MODE_BOTH, stream=None):
-    """wv_residues_device on a torch uint64/int64 cuda tensor of primes -> (res_w, res_v) tensors."""
+def residues_device(primes, mode=MODE_BOTH, stream=None, max_p=None):
+    """wv_residues_device on a torch uint64/int64 cuda tensor of primes -> (res_w, res_v) tensors.
+    The workspace is sized for primes <= max_p (default: the list's maximum; a smaller bound only
+    drops the coarse seg index for the larger primes, which then scan their sums)."""
     import torch
     n = primes.numel()
+    if max_p is None:
+        max_p = int(primes.max().item()) if n else 0
     ws = ctypes.c_size_t()
-    _check(lib().wv_residues_workspace_bytes(n, 0, mode, ctypes.byref(ws)))
+    _check(lib().wv_residues_workspace_bytes(n, max_p, mode, ctypes.byref(ws)))
     work = torch.empty(max(int(ws.value), 1), dtype=torch.uint8, device=primes.device)
     rw = torch.empty_like(primes)
     rv = torch.empty_like(primes)

@@ -296,6 +296,26 @@ def test_c4_c5_sampled_primes(wv, name):
     assert (int(res["res_w"][0]) if w.mode & 1 else NONE) == int(gw[0])
 
 
+@pytest.mark.gpu
+def test_coarse_seg_index_fallback(wv):
+    """Sum-aligned (> 96-sum) congruences locate a chunk's sum through a coarse per-record index
+    sized by the workspace.  The C4/C5 samples (BG_BIG / EG_BIG, ~3500 sums) with a workspace for
+    primes <= 2^30 (no room for their index: every record scans its sums) and with the full
+    index give the same, oracle-exact residues."""
+    import torch
+    for name in ("c4", "c5"):
+        gp, gw, gv, meta = _golden(name)
+        w = CONFIGS[name]
+        t = torch.tensor(gp.astype(np.int64), device="cuda")
+        small = [x.cpu().numpy().view(np.uint64) for x in wv.residues_device(t, w.mode, max_p=1 << 30)]
+        full = [x.cpu().numpy().view(np.uint64) for x in wv.residues_device(t, w.mode)]
+        for got in (small, full):
+            if w.mode & 1:
+                _assert_equal(gp, got[0], gw, f"{name} W")
+            if w.mode & 2:
+                _assert_equal(gp, got[1], gv, f"{name} V")
+
+
 # ---------------------------------------------------------------- NEXT-1: near misses and histograms
 def _near_window(wv, lo, hi, mode, bound=50):
     ds = wv.DeviceSearch(lo, hi, mode).run()
