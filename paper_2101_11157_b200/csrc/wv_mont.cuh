@@ -46,8 +46,8 @@ struct Mont32 {
         uint32_t s = a + b;                     // < 4p < 2^32
         return min(s, s - p2);
     }
-    // (a b + c d) R^{-1} mod p in [0, 2p) with one REDC: a, b, c, d < 2p, so
-    // T < 8p^2 and T + m p < 2^63 + 2^62; the REDC output is < 3p.
+    // (a b + c d) R^{-1} mod p in [0, 2p) with one REDC: a, b, c < 2p and d < 4p, so
+    // T < 12p^2 and T + m p < 3 2^62 + 2^62 = 2^64; the REDC output is < 4p.
     __device__ __forceinline__ uint32_t mul2add(uint32_t a, uint32_t b, uint32_t c, uint32_t d) const {
         uint64_t T = (uint64_t)a * b + (uint64_t)c * d;
         uint32_t m = (uint32_t)T * pinv;

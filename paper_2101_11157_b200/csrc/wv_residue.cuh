@@ -245,26 +245,30 @@ __device__ __forceinline__ uint64_t find_rec_warp(const uint64_t *__restrict__ s
 //                the DFMA pipe, balanced values, periodic range reduction.
 template <class M, int E>
 struct Run {
+    // u = s^E is kept as a plain residue (lazy [0, 2p)), not in Montgomery form.  The products
+    // a1 <- REDC(a1 u + a0 R), a0 <- REDC(a0 u) then scale the ratio a1/a0 by R at every term
+    // (a1/a0 -> a1/a0 + R/u), so result() returns c1 = a1 R^{-1}.  For E = 2 this makes
+    // d1 = 2s + 1 (< 2p) and d2 = 2 plain integers that never need a reduction.
     using W = typename M::W;
     static constexpr bool kFP = false;
     W u, d1, d2, d3, a0, a1;
     __device__ __forceinline__ void setup(const M &mo, const ModD &, uint64_t s0) {   // s0 < p
-        const W sm = mo.mul((W)s0, mo.r2);
+        const W sm = mo.mul((W)s0, mo.r2);                         // s R
+        const W s2m = mo.mul(sm, sm);                              // s^2 R
+        const W s = (W)s0;
         if (E == 3) {
-            const W s2 = mo.mul(sm, sm);
-            u = mo.mul(s2, sm);
+            u = mo.mul(mo.mul(s2m, sm), (W)1);                     // s^3
+            const W s2 = mo.mul(s2m, (W)1);                        // s^2
             const W s2x3 = mo.add(mo.add(s2, s2), s2);
-            const W smx3 = mo.add(mo.add(sm, sm), sm);
-            d1 = mo.add(mo.add(s2x3, smx3), mo.r1);                  // 3s^2 + 3s + 1
-            const W smx6 = mo.add(smx3, smx3);
-            const W r1x3 = mo.add(mo.add(mo.r1, mo.r1), mo.r1);
-            const W r1x6 = mo.add(r1x3, r1x3);
-            d2 = mo.add(smx6, r1x6);                                  // 6s + 6
-            d3 = r1x6;                                                // 6
+            const W sx3 = mo.add(mo.add(s, s), s);
+            d1 = mo.add(mo.add(s2x3, sx3), (W)1);                  // 3s^2 + 3s + 1
+            const W sx6 = mo.add(sx3, sx3);
+            d2 = mo.add(sx6, (W)6);                                // 6s + 6
+            d3 = 6;
         } else {
-            u = mo.mul(sm, sm);
-            d1 = mo.add(mo.add(sm, sm), mo.r1);                       // 2s + 1
-            d2 = mo.add(mo.r1, mo.r1);                                // 2
+            u = mo.mul(s2m, (W)1);                                 // s^2
+            d1 = 2 * s + 1;                                        // 2s + 1 < 2p, plain
+            d2 = 2;
             d3 = 0;
         }
         a0 = mo.r1;
@@ -275,21 +279,34 @@ struct Run {
         a1 = mo.muladd(a1, u, a0);
         a0 = mo.mul(a0, u);
         u = mo.add(u, d1);
-        d1 = mo.add(d1, d2);
-        if (E == 3) d2 = mo.add(d2, d3);
+        if (E == 3) {
+            d1 = mo.add(d1, d2);
+            d2 = mo.add(d2, d3);
+        } else {
+            d1 += d2;
+        }
     }
     // two terms at once: 1/u1 + 1/u2 = (u1 + u2) / (u1 u2), so with D = u1 u2, N = u1 + u2:
     //   a1 <- a1 D + a0 N  (one REDC for both products),  a0 <- a0 D
-    // 5 Montgomery-product halves instead of 6 for the pair (PAIRS engines only).
+    // 5 Montgomery-product halves instead of 6 for the pair (PAIRS engines only).  For Mont32
+    // N < 4p is left unreduced (mul2add: 2p 2p + 2p 4p + m p < 2^64 for p < 2^30).
     __device__ __forceinline__ void step2(const M &mo, const ModD &) {
         const W u2 = mo.add(u, d1);
-        d1 = mo.add(d1, d2);
-        if (E == 3) d2 = mo.add(d2, d3);
-        const W N = mo.add(u, u2);
+        if (E == 3) {
+            d1 = mo.add(d1, d2);
+            d2 = mo.add(d2, d3);
+        } else {
+            d1 += d2;
+        }
+        const W N = sizeof(W) == 4 ? u + u2 : mo.add(u, u2);     // Mont64 (p up to 2^62): reduce
         const W D = mo.mul(u, u2);
         u = mo.add(u2, d1);
-        d1 = mo.add(d1, d2);
-        if (E == 3) d2 = mo.add(d2, d3);
+        if (E == 3) {
+            d1 = mo.add(d1, d2);
+            d2 = mo.add(d2, d3);
+        } else {
+            d1 += d2;
+        }
         a1 = mo.mul2add(a1, D, a0, N);
         a0 = mo.mul(a0, D);
     }
@@ -300,11 +317,18 @@ struct Run {
         a1 = act ? n1 : a1;
         a0 = act ? n0 : a0;
         u = mo.add(u, d1);
-        d1 = mo.add(d1, d2);
-        if (E == 3) d2 = mo.add(d2, d3);
+        if (E == 3) {
+            d1 = mo.add(d1, d2);
+            d2 = mo.add(d2, d3);
+        } else {
+            d1 += d2;
+        }
     }
     __device__ __forceinline__ void reduce(const ModD &) {}
-    __device__ __forceinline__ void result(const M &, const ModD &, W &c0, W &c1) const { c0 = a0; c1 = a1; }
+    __device__ __forceinline__ void result(const M &mo, const ModD &, W &c0, W &c1) const {
+        c0 = a0;
+        c1 = mo.mul(a1, (W)1);                   // undo the factor R the plain u puts on a1/a0
+    }
     // sum-start state (u, d1, d2) to / from shared memory; coefficient rescaling at a sum switch
     __device__ __forceinline__ void save_start(uint64_t *st) const { st[0] = u; st[1] = d1; st[2] = d2; }
     __device__ __forceinline__ void load_start(const uint64_t *st) { u = (W)st[0]; d1 = (W)st[1]; d2 = (W)st[2]; }
