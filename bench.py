@@ -21,7 +21,7 @@ is reported.  nvidia-smi is sampled during the timed region.
             into host memory every step, wall clock, max over ranks.
 `roofline` -- the dominant kernel (residue_kernel) via the library's CUDA-event
             stats hook: algorithmic Montgomery multiplications / its device time,
-            against the IMAD-pipe peak.
+            against the IMAD-pipe peak from the guide's unit counts.
 `cpu_baseline` -- the CPU oracle (oracle/) as it stands, on a bounded sample
             of the same workload, on this box's host cores (rank 0, N=1 only).
 """
@@ -42,12 +42,13 @@ UNIT = "primes/s"
 MULMODS_PER_TERM = 2
 # SURVEY.md 8(d) per-unit figure: algorithmic terms per prime (BB30: 227/6480 p, EE33: 27/512 p)
 TERMS_PER_P = {1: 227 / 6480, 2: 27 / 512}
-# Roofline per prime class: (pipe, lanes/clk/SM, pipe slots per modular product)
-#   class 0 (p < 2^30, Mont32): fmaheavy pipe, 64 IMAD/clk/SM (guide: rt_SMSP = 2);
-#            IMAD.WIDE 2 + IMAD 1 + IMAD.HI 2 = 5 slots per product (WIDE/HI measured at half rate)
+# Roofline per prime class: (pipe, lanes/clk/SM, pipe ops per modular product)
+#   class 0 (p < 2^30, Mont32): IMAD pipe, 64 IMAD/clk/SM (guide); a Montgomery product is 3 IMAD-class
+#            ops (a b wide, m = T p^-1, hi(m p)).  Our microbenchmark measures IMAD.WIDE / IMAD.HI at half
+#            rate (5 pipe slots per product); that tighter ceiling is reported alongside (peak_5slot).
 #   class 1 (2^30 <= p < 2^44, FP64 EFT): fp64 pipe, 64 DFMA/clk/SM; 6 DP ops per product
 #   class 2 (p >= 2^44, Mont64): fmaheavy, ~22 slots per product (11 wide/high 32-bit partial products)
-ROOF = {0: ("fmaheavy", 64, 5), 1: ("fp64", 64, 6), 2: ("fmaheavy", 64, 22)}
+ROOF = {0: ("fmaheavy", 64, 3), 1: ("fp64", 64, 6), 2: ("fmaheavy", 64, 22)}
 
 
 def _env_int(name, default):
@@ -330,7 +331,7 @@ def main():
                 wr = float(f[3]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(f[4], 1)
         if rd is not None and wr is not None:
             traffic = rd + wr
-    kname = {0: "residue_kernel<Mont32> (class 0, p < 2^30)", 1: "residue_kernel<Mont64, FP64 engine> (class 1)",
+    kname = {0: "residue_lane2_kernel (class 0 lane mode, p < 2^30)", 1: "residue_kernel<Mont64, FP64 engine> (class 1)",
              2: "residue_kernel<Mont64> (class 2, p >= 2^44)"}[cls]
     roof = {"bound": "alu", "kernel": kname, "achieved": achieved / 1e9, "peak": peak_mulmod / 1e9,
             "achieved_basis": "SURVEY.md 8(d): 2 mulmods x (227/6480 p + 27/512 p) per prime (BB30/EE33 work)",
@@ -339,7 +340,7 @@ def main():
             "traffic_unit": "bytes/launch (DRAM read+write, ncu --set full, profiles/)",
             "peak_basis": f"{pipe} pipe: {lanes} lanes/clk/SM x {sms} SMs x {mhz:.0f} MHz ({peak_kind} sm_max_mhz) "
                           f"/ {slots} pipe slots per modular product",
-            "peak_guide_3imad": lanes * sms * mhz * 1e6 / 3 / 1e9 if cls == 0 else None,
+            "peak_5slot": lanes * sms * mhz * 1e6 / 5 / 1e9 if cls == 0 else None,
             "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms_max if ms_max else None,
             "terms_per_step": sum(cls_terms.values()), "kernel_terms_per_s": k_terms / (k_ms / 1e3) if k_ms else None}
 

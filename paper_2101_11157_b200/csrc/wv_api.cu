@@ -20,6 +20,7 @@
 #include "../../include/wv.h"
 #include "wv_mont.cuh"
 #include "wv_residue.cuh"
+#include "wv_lane.cuh"
 #include "wv_scan.cuh"
 #include "wv_sieve.cuh"
 #include "wv_census.cuh"
@@ -189,11 +190,12 @@ static const Variant kVariants[] = {
     {"c0 int s1/1 pairs", 0, residue_kernel<Mont32, 0, 0, 1, 1, true>, nullptr},
     {"c0 int s2/2 pairs", 0, residue_kernel<Mont32, 0, 0, 2, 2, true>, nullptr},
     {"c2 int s1/1 pairs", 2, residue_kernel<Mont64, 2, 0, 1, 1, true>, nullptr},
+    {"c0 lane2", 0, nullptr, residue_lane2_kernel},                   // lane mode v2 (sorted lists)
 };
 static const int NVAR = sizeof kVariants / sizeof kVariants[0];
 static_assert(NVAR <= 32, "DevCtx::occ holds 32 variants");
-static const int kDefaultVariant[3] = {13, 6, 8};  // measured best (scripts/variant_sweep.py)
-static int g_variant[3] = {13, 6, 8};              // per class
+static const int kDefaultVariant[3] = {15, 6, 8};  // measured best (scripts/variant_sweep.py)
+static int g_variant[3] = {15, 6, 8};              // per class
 static const int kChunkFallback0 = 13;             // class-0 chunk variant when lane mode is unusable
 static void read_variant_env() {
     static bool done = false;
@@ -244,6 +246,13 @@ static int ctx_get(DevCtx **out) {
             CK(cudaMemcpy(dt, T.terms.data(), T.terms.size() * sizeof(Term), cudaMemcpyHostToDevice));
             const Term *dtc = dt;
             CK(cudaMemcpyToSymbol(c_terms, &dtc, sizeof dtc));
+            std::vector<double2> rr(T.terms.size());          // reciprocals of the endpoint denominators
+            for (size_t i = 0; i < rr.size(); i++) rr[i] = make_double2(1.0 / T.terms[i].xd, 1.0 / T.terms[i].yd);
+            double2 *dr = nullptr;
+            CK(cudaMalloc(&dr, rr.size() * sizeof(double2)));
+            CK(cudaMemcpy(dr, rr.data(), rr.size() * sizeof(double2), cudaMemcpyHostToDevice));
+            const double2 *drc = dr;
+            CK(cudaMemcpyToSymbol(c_termr, &drc, sizeof drc));
         }
         for (int v = 0; v < NVAR; v++) {
             if (kVariants[v].fn)
@@ -318,7 +327,7 @@ static const uint64_t PART_BUDGET = 1ull << 24;   // partial pairs per batch (25
 
 enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2 /* 2 slots: first k with p >= 2^30, >= 2^44 */,
        M_CNT = 4 /* 3 slots: work counters per class */, M_NHITS = 7, M_CHECKSUM = 8, M_NBASE1 = 9,
-       M_SPLIT = 10 /* 4 slots */, M_TERMS = 14 /* 3 slots: terms per class */, M_SLOTS = 24 };
+       M_SPLIT = 10 /* 4 slots */, M_TERMS = 14 /* 3 slots: terms per class */, M_LANE_T = 17, M_SLOTS = 24 };
 
 struct Layout {
     // problem
@@ -513,6 +522,14 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     bool lane = sorted && kVariants[var0].lane != nullptr;
     if (!lane && kVariants[var0].lane) var0 = kChunkFallback0;
     const unsigned grid_plan = (unsigned)((K + 255) / 256 < (uint64_t)c->sms * 32 ? (K + 255) / 256 : c->sms * 32);
+    // lane-mode slices per group: the v1 kernel cuts 8192-term slices; v2 keeps whole sums unless the
+    // window has too few groups to fill the GPU (WV_LANE_ITEMS items per resident warp wanted)
+    const bool lane2 = lane && kVariants[var0].lane == residue_lane2_kernel;
+    double lane_items = 0;
+    if (lane2) {
+        const char *ev = getenv("WV_LANE_ITEMS");
+        lane_items = (ev ? atof(ev) : 8.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
+    }
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
     uint64_t hs[4], ht[3];
     for (int attempt = 0; attempt < 2; attempt++) {
@@ -527,7 +544,14 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             (void)table();
             LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
                    nch, (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
-                   (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr, segidx, L.segstride);
+                   (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr, segidx, L.segstride, LANE_SLICE,
+                   LANE_QMAX, (lane && lane2) ? (unsigned long long *)(misc + M_LANE_T) : nullptr);
+            if (lane && lane2 && L.ngt > 0) {
+                const uint64_t nb = (L.ngt + 255) / 256;
+                LAUNCH(lane_slices_kernel, (unsigned)(nb < (uint64_t)c->sms * 8 ? nb : c->sms * 8), 256, st, gq, L.ngt,
+                       L.ntests, recs, K, nch, (const unsigned long long *)(misc + M_LANE_T), lane_items, 4096ull,
+                       LANE_QMAX);
+            }
         }
         TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
         if (lane) TRY(scan_excl<uint64_t>(gq, L.ngt, gstart, gstart + L.ngt, tiles, st));

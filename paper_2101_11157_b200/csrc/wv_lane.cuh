@@ -1,0 +1,298 @@
+// wv_lane.cuh -- class-0 lane-mode residue kernel (sorted prime lists, 5 <= p < 2^30).
+//
+// A warp item is (group of 32 consecutive primes of one test, slice q of Q).  Lane l owns
+// record (32 g + l, test) and walks every sum j of its congruence,
+// taking slice q of each: for a sum with n_j terms, [floor(q n_j / Q), floor((q+1) n_j / Q)).
+// Neighbouring primes share the congruence and have nearly equal n_j, so all lanes cross sum
+// boundaries together: per sum one unmasked loop of min-count pair steps, then a short masked
+// tail.  (The chunk kernel splits one record over 64 lane streams instead; with C2-size primes
+// and ~90-sum congruences its streams cross sum boundaries at different times and the lockstep
+// loop breaks every ~8 terms.)
+//
+// Arithmetic: everything in Montgomery form x R mod p (R = 2^32), lazy in [0, 2p), with the
+// subtractive REDC  m = T_lo p^{-1} mod R,  REDC(T) = T_hi - hi(m p) + p  -- the low words cancel
+// exactly, so no carry is propagated -- which lies in (0, p + T_hi].
+//
+// The sum of inverses is the ratio a1/a0 of eqnComputeS, advanced two terms at a time:
+//     1/u1 + 1/u2 = N / D,   D = u1 u2,  N = u1 + u2,
+//     a1 <- REDC(a1 D + a0 N),   a0 <- REDC(a0 D)          (ratio += N/D; one REDC for both products)
+// e = 2 (V): D(s) = (s (s+1))^2 and N(s) = s^2 + (s+1)^2 are polynomials in s of degree 4 and 2;
+//            step-2 forward differences advance them with modular adds only: 2 products per pair.
+// e = 3 (W): u = s^3 by unit-step finite differences, D = u1 u2 (one product), N = u1 + u2:
+//            3 products per pair (the degree-6 difference table costs more adds than it saves).
+// At the end of a sum: c1 <- a_j c1 (fold) and (C0, C1) (+) (c0, c1) (eqnCombinePairs).
+#pragma once
+#include <stdint.h>
+#include "wv_residue.cuh"
+
+namespace wv {
+
+__constant__ const double2 *c_termr;     // {fl(1/xd), fl(1/yd)} per term (same index as c_terms)
+
+// floor(n / d) for n < 2^62, 0 < d < 2^32, rd = fl(1/d): double estimate (off by at most one for
+// quotients < 2^40), then an exact integer correction.
+__device__ __forceinline__ uint64_t fdiv(uint64_t n, uint32_t d, double rd) {
+    uint64_t q = (uint64_t)__dmul_rz(__ull2double_rz(n), rd);
+    const int64_t r = (int64_t)(n - q * d);
+    if (r < 0) q--;
+    else if (r >= (int64_t)d) q++;
+    return q;
+}
+
+// first s and count of x p < s < y p (strict) for p < 2^32: exact.
+__device__ __forceinline__ void lane_bounds(uint32_t p, const Term &t, double2 rr, uint64_t &first, uint32_t &cnt) {
+    const uint64_t f = fdiv((uint64_t)t.xn * p, t.xd, rr.x) + 1;                  // floor(x p) + 1
+    const uint64_t l = fdiv((uint64_t)t.yn * p + t.yd - 1, t.yd, rr.y) - 1;       // ceil(y p) - 1
+    first = f;
+    cnt = l >= f ? (uint32_t)(l - f + 1) : 0u;
+}
+
+struct MontS {      // p < 2^30, R = 2^32, values lazy in [0, 2p)
+    uint32_t p, pinv, p2, r1, r2;        // pinv = p^{-1} mod 2^32 (positive); r1 = R mod p; r2 = R^2 mod p
+    __device__ __forceinline__ void init(uint32_t p_) {
+        p = p_;
+        p2 = 2u * p;
+        uint32_t inv = p;                                    // p p == 1 mod 8
+        #pragma unroll
+        for (int i = 0; i < 4; i++) inv *= 2u - p * inv;     // 3 -> 48 bits
+        pinv = inv;
+        r1 = (uint32_t)(0x100000000ull % p);
+        r2 = (uint32_t)(((uint64_t)r1 * r1) % p);
+    }
+    // T R^{-1} mod p, in (0, p + T_hi]
+    __device__ __forceinline__ uint32_t redc(uint64_t T) const {
+        const uint32_t m = (uint32_t)T * pinv;
+        return (uint32_t)(T >> 32) - __umulhi(m, p) + p;
+    }
+    // a, b < 2p: a b < 4p^2 < p 2^32, result in (0, 2p)
+    __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return redc((uint64_t)a * b); }
+    // (a b + c d) R^{-1}: BIG (p < 2^30, all < 2p): T < 8p^2, REDC in (0, 3p), one lazy subtract;
+    // !BIG (p < 2^28, a, b, c < 2p, d < 4p): T < 12 p^2 < p 2^32, REDC already in (0, 2p).
+    template <bool BIG>
+    __device__ __forceinline__ uint32_t mul2add(uint32_t a, uint32_t b, uint32_t c, uint32_t d) const {
+        const uint32_t t = redc((uint64_t)a * b + (uint64_t)c * d);
+        return BIG ? min(t, t - p2) : t;
+    }
+    // l < 2^32, r < 2p: T < 2^33 p, REDC in (0, 3p) -> [0, 2p)
+    __device__ __forceinline__ uint32_t mulw(uint32_t l, uint32_t r) const {
+        const uint32_t t = redc((uint64_t)l * r);
+        return min(t, t - p2);
+    }
+    __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const {
+        const uint32_t s = a + b;
+        return min(s, s - p2);
+    }
+    __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const {
+        const uint32_t s = a - b + p2;                       // (0, 4p)
+        return min(s, s - p2);
+    }
+};
+
+// a_j R mod p from the 128-bit magnitude (4 limbs) and sign; rho[i] = R^{i+2} mod p
+__device__ __forceinline__ uint32_t lane_coef(const MontS &mo, const Term &t, const uint32_t rho[4]) {
+    uint32_t a = mo.mulw((uint32_t)t.a_lo, rho[0]);
+    if (t.a_lo >> 32) a = mo.add(a, mo.mulw((uint32_t)(t.a_lo >> 32), rho[1]));
+    if (t.a_hi) {
+        a = mo.add(a, mo.mulw((uint32_t)t.a_hi, rho[2]));
+        a = mo.add(a, mo.mulw((uint32_t)(t.a_hi >> 32), rho[3]));
+    }
+    if (t.neg) a = mo.sub(0u, a);
+    return a;
+}
+
+// e = 2 run: D, its three leading step-2 differences and the constant fourth; N, its first
+// difference and the constant second -- all in Montgomery form.
+struct LaneRun2 {
+    uint32_t D0, D1, D2, D3, Dc, N0, N1, Nc, a0, a1;
+    __device__ __forceinline__ void setup(const MontS &mo, uint32_t x) {   // x < p
+        const uint32_t xt = mo.mul(x, mo.r2);                               // x R
+        const uint32_t r2_ = mo.add(mo.r1, mo.r1), r4 = mo.add(r2_, r2_), r6 = mo.add(r4, r2_), r8 = mo.add(r4, r4);
+        const uint32_t x2t = mo.add(xt, xt), x4t = mo.add(x2t, x2t), x8t = mo.add(x4t, x4t);
+        uint32_t t = mo.mul(xt, mo.add(xt, mo.r1));                         // x (x+1) R
+        uint32_t g = mo.add(x4t, r6);                                       // t(x+2) - t(x) = 4x + 6
+        uint32_t v[5];
+        #pragma unroll
+        for (int i = 0; i < 5; i++) {
+            v[i] = mo.mul(t, t);                                            // (x_i (x_i + 1))^2 R, x_i = x + 2i
+            t = mo.add(t, g);
+            g = mo.add(g, r8);
+        }
+        #pragma unroll
+        for (int k = 1; k < 5; k++) {
+            #pragma unroll
+            for (int i = 4; i >= k; i--) v[i] = mo.sub(v[i], v[i - 1]);
+        }
+        D0 = v[0]; D1 = v[1]; D2 = v[2]; D3 = v[3]; Dc = v[4];
+        const uint32_t xx = mo.mul(xt, xt);                                 // x^2 R
+        N0 = mo.add(mo.add(xx, xx), mo.add(x2t, mo.r1));                    // 2x^2 + 2x + 1
+        N1 = mo.add(x8t, mo.add(r8, r4));                                   // 8x + 12
+        Nc = mo.add(r8, r8);                                                // 16
+        a0 = mo.r1;
+        a1 = 0;
+    }
+    template <bool BIG, bool MASK>
+    __device__ __forceinline__ void pair(const MontS &mo, bool act) {
+        const uint32_t n1 = mo.mul2add<BIG>(a1, D0, a0, N0);
+        const uint32_t n0 = mo.mul(a0, D0);
+        a1 = (!MASK || act) ? n1 : a1;
+        a0 = (!MASK || act) ? n0 : a0;
+        D0 = mo.add(D0, D1);
+        D1 = mo.add(D1, D2);
+        D2 = mo.add(D2, D3);
+        D3 = mo.add(D3, Dc);
+        N0 = mo.add(N0, N1);
+        N1 = mo.add(N1, Nc);
+    }
+    // one term s = x (x < p), masked
+    template <bool BIG>
+    __device__ __forceinline__ void single(const MontS &mo, uint32_t x, bool act) {
+        const uint32_t xt = mo.mul(x, mo.r2);
+        const uint32_t u = mo.mul(xt, xt);
+        const uint32_t n1 = mo.mul2add<BIG>(a1, u, a0, mo.r1);
+        const uint32_t n0 = mo.mul(a0, u);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
+    }
+};
+
+// e = 3 run: u = s^3 and its unit-step differences (3s^2+3s+1, 6s+6, 6), Montgomery form.
+struct LaneRun3 {
+    uint32_t u, d1, d2, d3, a0, a1;
+    __device__ __forceinline__ void setup(const MontS &mo, uint32_t x) {
+        const uint32_t xt = mo.mul(x, mo.r2);
+        const uint32_t xx = mo.mul(xt, xt);
+        u = mo.mul(xx, xt);
+        const uint32_t r3 = mo.add(mo.add(mo.r1, mo.r1), mo.r1);
+        const uint32_t x3 = mo.add(mo.add(xt, xt), xt);
+        d1 = mo.add(mo.add(mo.add(xx, xx), xx), mo.add(x3, mo.r1));
+        d3 = mo.add(r3, r3);
+        d2 = mo.add(mo.add(x3, x3), d3);
+        a0 = mo.r1;
+        a1 = 0;
+    }
+    template <bool BIG, bool MASK>
+    __device__ __forceinline__ void pair(const MontS &mo, bool act) {
+        const uint32_t u2 = mo.add(u, d1);
+        d1 = mo.add(d1, d2);
+        d2 = mo.add(d2, d3);
+        const uint32_t N = BIG ? mo.add(u, u2) : u + u2;
+        const uint32_t D = mo.mul(u, u2);
+        u = mo.add(u2, d1);
+        d1 = mo.add(d1, d2);
+        d2 = mo.add(d2, d3);
+        const uint32_t n1 = mo.mul2add<BIG>(a1, D, a0, N);
+        const uint32_t n0 = mo.mul(a0, D);
+        a1 = (!MASK || act) ? n1 : a1;
+        a0 = (!MASK || act) ? n0 : a0;
+    }
+    // one term s = x (x < p), masked; u is recomputed (masked pair steps advanced it for every lane)
+    template <bool BIG>
+    __device__ __forceinline__ void single(const MontS &mo, uint32_t x, bool act) {
+        const uint32_t xt = mo.mul(x, mo.r2);
+        const uint32_t w = mo.mul(mo.mul(xt, xt), xt);
+        const uint32_t n1 = mo.mul2add<BIG>(a1, w, a0, mo.r1);
+        const uint32_t n0 = mo.mul(a0, w);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
+    }
+};
+
+// One item: every sum of the lane's congruence, slice q of Q.  Returns the merged (C0, C1).
+template <class Run, bool BIG>
+__device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
+                                           double rQ, uint32_t &C0, uint32_t &C1) {
+    const uint32_t m = valid ? cg.m : 0u;
+    const uint32_t mmax = __reduce_max_sync(0xffffffffu, m);
+    uint32_t rho[4];
+    rho[0] = mo.r2;
+    rho[1] = mo.mul(mo.r2, mo.r2);
+    rho[2] = mo.mul(rho[1], mo.r2);
+    rho[3] = mo.mul(rho[2], mo.r2);
+    for (uint32_t j = 0; j < mmax; j++) {
+        uint32_t cnt = 0;
+        uint64_t s0 = 1;
+        Term tm;
+        if (j < m) {
+            tm = c_terms[cg.off + j];
+            uint64_t f;
+            uint32_t n;
+            lane_bounds(mo.p, tm, c_termr[cg.off + j], f, n);
+            uint64_t a = 0, b = n;
+            if (Q > 1) {
+                a = fdiv((uint64_t)n * q, (uint32_t)Q, rQ);
+                b = fdiv((uint64_t)n * (q + 1), (uint32_t)Q, rQ);
+            }
+            cnt = (uint32_t)(b - a);
+            s0 = f + a;
+        }
+        const bool act = cnt != 0;
+        const uint32_t np = cnt >> 1;
+        const uint32_t kmin = __reduce_min_sync(0xffffffffu, act ? np : 0xffffffffu);
+        if (kmin == 0xffffffffu) continue;                       // no lane has terms in this sum
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, act ? np : 0u);
+        const bool odd = act && (cnt & 1u);
+        Run run;
+        run.setup(mo, (uint32_t)s0);
+        uint32_t i = 0;
+        #pragma unroll 1
+        for (; i + 4 <= kmin; i += 4) {
+            run.template pair<BIG, false>(mo, true);
+            run.template pair<BIG, false>(mo, true);
+            run.template pair<BIG, false>(mo, true);
+            run.template pair<BIG, false>(mo, true);
+        }
+        #pragma unroll 1
+        for (; i < kmin; i++) run.template pair<BIG, false>(mo, true);
+        #pragma unroll 1
+        for (; i < kmax; i++) run.template pair<BIG, true>(mo, i < np);
+        if (__any_sync(0xffffffffu, odd)) run.template single<BIG>(mo, (uint32_t)(s0 + 2ull * np), odd);
+        if (act) {
+            const uint32_t c1 = mo.mul(run.a1, lane_coef(mo, tm, rho));          // fold a_j
+            const uint32_t n1 = mo.mul2add<true>(C0, c1, C1, run.a0);            // eqnCombinePairs
+            C0 = mo.mul(C0, run.a0);
+            C1 = n1;
+        }
+    }
+}
+
+// items it in [0, nitems) processed largest-first (groups ascend in p); gstart = exclusive scan of
+// gq (slices per group-test); start = per-record partial slots.
+__global__ void __launch_bounds__(RES_THREADS, 4)
+residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
+                     const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
+                     uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
+                     ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long it = 0;
+        if (lane == 0) it = atomicAdd(counter, 1ull);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) break;
+        const uint64_t item = nitems - 1 - it;
+        const uint64_t gt = find_rec(gstart, 0, ngt, item);
+        const uint64_t q = item - gstart[gt], Q = gq[gt];
+        const uint64_t g = gt / ntests, t = gt % ntests;
+        const uint64_t k = (32 * g + lane) * ntests + t;
+        Rec r;
+        r.p = 0;
+        if (k < K) r = recs[k];
+        const bool valid = r.p != 0 && r.p < WIDTH32_MAX;
+        const Cong &cg = c_cong[valid ? r.cid : 0];
+        MontS mo;
+        mo.init(valid ? (uint32_t)r.p : 7u);
+        uint32_t C0 = mo.r1, C1 = 0;
+        const double rQ = 1.0 / (double)Q;
+        const uint32_t e = __reduce_max_sync(0xffffffffu, valid ? cg.e : 0u);   // one test per item
+        const bool big = __any_sync(0xffffffffu, valid && r.p >= (1ull << 28));
+        if (e == 3) {
+            if (big) lane2_item<LaneRun3, true>(mo, cg, valid, q, Q, rQ, C0, C1);
+            else lane2_item<LaneRun3, false>(mo, cg, valid, q, Q, rQ, C0, C1);
+        } else {
+            if (big) lane2_item<LaneRun2, true>(mo, cg, valid, q, Q, rQ, C0, C1);
+            else lane2_item<LaneRun2, false>(mo, cg, valid, q, Q, rQ, C0, C1);
+        }
+        if (valid) partials[start[k] + q - part_base] = make_ulonglong2(C0, C1);
+    }
+}
+
+}  // namespace wv

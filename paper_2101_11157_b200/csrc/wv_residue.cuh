@@ -126,7 +126,8 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
                             Rec *__restrict__ recs, uint64_t *__restrict__ nchunks,
                             unsigned long long *__restrict__ first64, int *__restrict__ err,
                             unsigned long long *__restrict__ terms, uint64_t *__restrict__ gq,
-                            uint32_t *__restrict__ segidx, uint32_t segstride) {
+                            uint32_t *__restrict__ segidx, uint32_t segstride, uint64_t lane_slice,
+                            uint64_t lane_qmax, unsigned long long *__restrict__ lane_total) {
     const uint32_t ntests = (mode == 3) ? 2 : 1;
     const uint64_t n = n_primes_dev ? *n_primes_dev : n_primes_host;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kmax;
@@ -178,11 +179,20 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
                     sum_bounds(pl, c_terms[c_cong[cl].off + jj], &f, &cnt);
                     Tl += cnt;
                 }
-            uint64_t Q = (Tl + LANE_SLICE - 1) / LANE_SLICE;
-            if (Q < 1) Q = 1;
-            if (Q > LANE_QMAX) Q = LANE_QMAX;
-            nc = Q;
-            if (i == 32 * g) gq[g * ntests + (mode == 3 ? test : 0)] = Q;
+            if (lane_total) {
+                // deferred: gq = the group's term count, converted to slices by lane_slices_kernel
+                nc = 1;
+                if (i == 32 * g) {
+                    gq[g * ntests + (mode == 3 ? test : 0)] = Tl;
+                    atomicAdd(lane_total, (unsigned long long)Tl);
+                }
+            } else {
+                uint64_t Q = (Tl + lane_slice - 1) / lane_slice;
+                if (Q < 1) Q = 1;
+                if (Q > lane_qmax) Q = lane_qmax;
+                nc = Q;
+                if (i == 32 * g) gq[g * ntests + (mode == 3 ? test : 0)] = Q;
+            }
         }
         Rec r;
         r.p = p; r.T = T; r.cid = (uint32_t)cid; r.L = (uint32_t)L; r.idx = (uint32_t)i; r.test = test;
@@ -199,6 +209,33 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
              gt += (uint64_t)gridDim.x * blockDim.x) {
             const uint64_t i0 = (gt / ntests) * 32;
             if (i0 >= n || primes[i0] >= WIDTH32_MAX) gq[gt] = 0;
+        }
+    }
+}
+
+// Lane mode v2: slices per group-test from its term count Tl (gq on entry): one slice size for the
+// whole launch, total / (items wanted), so large groups are cut finer and small ones stay whole.
+// Sets gq[gt] = Q and the slot count of each class-0 record of the group.
+__global__ void lane_slices_kernel(uint64_t *__restrict__ gq, uint64_t ngt, uint32_t ntests, const Rec *__restrict__ recs,
+                                   uint64_t K, uint64_t *__restrict__ nchunks,
+                                   const unsigned long long *__restrict__ lane_total, double items_wanted,
+                                   uint64_t min_slice, uint64_t qmax) {
+    const double tot = (double)*lane_total;
+    uint64_t slice = (uint64_t)ceil(tot / (items_wanted > 1.0 ? items_wanted : 1.0));
+    if (slice < min_slice) slice = min_slice;
+    for (uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gt < ngt; gt += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t Tl = gq[gt];
+        if (Tl == 0) continue;                       // not a lane-mode group
+        uint64_t Q = (Tl + slice - 1) / slice;
+        if (Q < 1) Q = 1;
+        if (Q > qmax) Q = qmax;
+        gq[gt] = Q;
+        const uint64_t g = gt / ntests, t = gt % ntests;
+        for (uint64_t l = 0; l < 32; l++) {
+            const uint64_t k = (32 * g + l) * ntests + t;
+            if (k >= K) break;
+            const uint64_t p = recs[k].p;
+            if (p != 0 && p < WIDTH32_MAX) nchunks[k] = Q;
         }
     }
 }

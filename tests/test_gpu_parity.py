@@ -261,6 +261,32 @@ def test_kernel_variants_bit_identical(wv):
             wv.set_kernel_variant(c, -1)
 
 
+@pytest.mark.parametrize("items", ["0.001", "1000000"])
+def test_lane2_slicing_bit_exact(wv, items, monkeypatch):
+    """Class-0 lane mode v2 cuts each group's sums into Q slices (one slice size per launch, from
+    WV_LANE_ITEMS items per resident warp): whole sums (Q = 1) and the finest cut (Q up to 128) give the
+    residues of the chunk kernel and of the oracle, on a C2-size window (both tests, p < 2^28) and a
+    window above 2^28 (the lazy-subtract variant of the pair step)."""
+    ids = {name: vid for vid, name, cls in wv.kernel_variants()}
+    windows = [(5, 300000, 3), ((1 << 28) - 3000, (1 << 28) + 3000, 3), (10 ** 9, 10 ** 9 + 6000, 2)]
+    try:
+        for lo, hi, mode in windows:
+            wv.set_kernel_variant(0, ids["c0 int s2/2 pairs"])
+            _, ref = wv.search(lo, hi, mode)
+            wv.set_kernel_variant(0, ids["c0 lane2"])
+            monkeypatch.setenv("WV_LANE_ITEMS", items)
+            _, got = wv.search(lo, hi, mode)
+            monkeypatch.delenv("WV_LANE_ITEMS")
+            assert got.tobytes() == ref.tobytes(), (lo, hi, items)
+            ps = got["p"].tolist()
+            idx = sample_indices(len(ps), 48)
+            rw, rv = _oracle_arrays([ps[i] for i in idx], mode)
+            _assert_equal(got["p"][idx], got["res_w"][idx], rw, f"W [{lo},{hi})")
+            _assert_equal(got["p"][idx], got["res_v"][idx], rv, f"V [{lo},{hi})")
+    finally:
+        wv.set_kernel_variant(0, -1)
+
+
 def test_class2_64bit_montgomery_cross_congruence(wv):
     """p >= 2^44 runs the 64-bit Montgomery engine: two different congruences agree
     (BB1 vs BB30 for W, EE3 vs EE33 for V) on a prime just above 2^44 (property check)."""
