@@ -50,8 +50,8 @@ struct GenTerm { uint32_t neg; uint64_t hi, lo; uint32_t xn, xd, yn, yd; };
 // generated-congruence tiers (name, test, threshold): names from congruences_gen.inc
 struct GenTier { const char *name; int test; uint64_t th; };
 static GenTier kGenTiers[] = {
-    {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 1ull << 29}, {"BG_BIG", 0, 1ull << 34},
-    {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 27}, {"EG_BIG", 1, 1ull << 32},
+    {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 1ull << 29}, {"BG_BIG", 0, 1ull << 24},
+    {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 27}, {"EG_BIG", 1, 1ull << 24},
 };
 
 // uniform host copy of every congruence: headers + one term array (uploaded per device)
@@ -107,6 +107,9 @@ static void sched_init(const Table &t) {
     for (GenTier &g : kGenTiers) {
         if (!strcmp(g.name, "BG_SML") && ew) g.th = strtoull(ew, nullptr, 0);
         if (!strcmp(g.name, "EG_SML") && ev) g.th = strtoull(ev, nullptr, 0);
+        char key[32];                                     // WV_TH_<tier name>: any tier's threshold
+        snprintf(key, sizeof key, "WV_TH_%s", g.name);
+        if (const char *e = getenv(key)) g.th = strtoull(e, nullptr, 0);
     }
     for (const GenTier &g : kGenTiers) {
         if (g.th == 0) continue;
@@ -528,7 +531,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     double lane_items = 0;
     if (lane2) {
         const char *ev = getenv("WV_LANE_ITEMS");
-        lane_items = (ev ? atof(ev) : 8.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
+        lane_items = (ev ? atof(ev) : 4.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
     }
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
     uint64_t hs[4], ht[3];

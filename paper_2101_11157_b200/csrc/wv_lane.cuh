@@ -103,6 +103,7 @@ __device__ __forceinline__ uint32_t lane_coef(const MontS &mo, const Term &t, co
 // e = 2 run: D, its three leading step-2 differences and the constant fourth; N, its first
 // difference and the constant second -- all in Montgomery form.
 struct LaneRun2 {
+    static constexpr uint32_t K = 2;                  // terms per step
     uint32_t D0, D1, D2, D3, Dc, N0, N1, Nc, a0, a1;
     __device__ __forceinline__ void setup(const MontS &mo, uint32_t x) {   // x < p
         const uint32_t xt = mo.mul(x, mo.r2);                               // x R
@@ -157,6 +158,7 @@ struct LaneRun2 {
 
 // e = 3 run: u = s^3 and its unit-step differences (3s^2+3s+1, 6s+6, 6), Montgomery form.
 struct LaneRun3 {
+    static constexpr uint32_t K = 2;
     uint32_t u, d1, d2, d3, a0, a1;
     __device__ __forceinline__ void setup(const MontS &mo, uint32_t x) {
         const uint32_t xt = mo.mul(x, mo.r2);
@@ -197,6 +199,71 @@ struct LaneRun3 {
     }
 };
 
+// e = 2 run, four terms per step: 1/u0 + 1/u1 + 1/u2 + 1/u3 = N / D with
+//     D(s) = (s (s+1) (s+2) (s+3))^2                      (degree 8)
+//     N(s) = u1 u2 u3 + u0 u2 u3 + u0 u1 u3 + u0 u1 u2       (degree 6),  u_i = (s+i)^2,
+// advanced by step-4 forward differences: per four terms the same 2 products (3 wide multiplies,
+// one shared REDC) as a pair step, plus 14 modular adds.  The tables are set up from D and N at
+// 9 and 7 points, N = P01 (u2 + u3) + P23 (u0 + u1) with P01 = u0 u1, P23 = u2 u3.
+struct LaneRun2Q {
+    static constexpr uint32_t K = 4;
+    uint32_t D0, D1, D2, D3, D4, D5, D6, D7, Dc, N0, N1, N2, N3, N4, N5, Nc, a0, a1;
+    __device__ __forceinline__ void setup(const MontS &mo, uint32_t x) {   // x < p
+        const uint32_t xt = mo.mul(x, mo.r2);
+        uint32_t u = mo.mul(xt, xt);                                        // s^2 R at s = x
+        uint32_t d1 = mo.add(mo.add(xt, xt), mo.r1);                        // (2s + 1) R
+        const uint32_t d2 = mo.add(mo.r1, mo.r1);                           // 2 R
+        uint32_t v[9], w[7];
+        #pragma unroll
+        for (int i = 0; i < 9; i++) {
+            uint32_t q[4];
+            #pragma unroll
+            for (int k = 0; k < 4; k++) {
+                q[k] = u;
+                u = mo.add(u, d1);
+                d1 = mo.add(d1, d2);
+            }
+            const uint32_t P01 = mo.mul(q[0], q[1]), P23 = mo.mul(q[2], q[3]);
+            v[i] = mo.mul(P01, P23);
+            if (i < 7) w[i] = mo.mul2add<true>(P01, mo.add(q[2], q[3]), P23, mo.add(q[0], q[1]));
+        }
+        #pragma unroll
+        for (int k = 1; k < 9; k++) {
+            #pragma unroll
+            for (int i = 8; i >= k; i--) v[i] = mo.sub(v[i], v[i - 1]);
+        }
+        #pragma unroll
+        for (int k = 1; k < 7; k++) {
+            #pragma unroll
+            for (int i = 6; i >= k; i--) w[i] = mo.sub(w[i], w[i - 1]);
+        }
+        D0 = v[0]; D1 = v[1]; D2 = v[2]; D3 = v[3]; D4 = v[4]; D5 = v[5]; D6 = v[6]; D7 = v[7]; Dc = v[8];
+        N0 = w[0]; N1 = w[1]; N2 = w[2]; N3 = w[3]; N4 = w[4]; N5 = w[5]; Nc = w[6];
+        a0 = mo.r1;
+        a1 = 0;
+    }
+    template <bool BIG, bool MASK>
+    __device__ __forceinline__ void pair(const MontS &mo, bool act) {       // one step = four terms
+        const uint32_t n1 = mo.mul2add<BIG>(a1, D0, a0, N0);
+        const uint32_t n0 = mo.mul(a0, D0);
+        a1 = (!MASK || act) ? n1 : a1;
+        a0 = (!MASK || act) ? n0 : a0;
+        D0 = mo.add(D0, D1); D1 = mo.add(D1, D2); D2 = mo.add(D2, D3); D3 = mo.add(D3, D4);
+        D4 = mo.add(D4, D5); D5 = mo.add(D5, D6); D6 = mo.add(D6, D7); D7 = mo.add(D7, Dc);
+        N0 = mo.add(N0, N1); N1 = mo.add(N1, N2); N2 = mo.add(N2, N3); N3 = mo.add(N3, N4);
+        N4 = mo.add(N4, N5); N5 = mo.add(N5, Nc);
+    }
+    template <bool BIG>
+    __device__ __forceinline__ void single(const MontS &mo, uint32_t x, bool act) {
+        const uint32_t xt = mo.mul(x, mo.r2);
+        const uint32_t w = mo.mul(xt, xt);
+        const uint32_t n1 = mo.mul2add<BIG>(a1, w, a0, mo.r1);
+        const uint32_t n0 = mo.mul(a0, w);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
+    }
+};
+
 // One item: every sum of the lane's congruence, slice q of Q.  Returns the merged (C0, C1).
 template <class Run, bool BIG>
 __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
@@ -226,11 +293,11 @@ __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool
             s0 = f + a;
         }
         const bool act = cnt != 0;
-        const uint32_t np = cnt >> 1;
+        const uint32_t np = cnt / Run::K;                        // steps of K terms, then cnt % K singles
         const uint32_t kmin = __reduce_min_sync(0xffffffffu, act ? np : 0xffffffffu);
         if (kmin == 0xffffffffu) continue;                       // no lane has terms in this sum
         const uint32_t kmax = __reduce_max_sync(0xffffffffu, act ? np : 0u);
-        const bool odd = act && (cnt & 1u);
+        const uint32_t rem = act ? cnt - np * Run::K : 0u;
         Run run;
         run.setup(mo, (uint32_t)s0);
         uint32_t i = 0;
@@ -245,7 +312,10 @@ __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool
         for (; i < kmin; i++) run.template pair<BIG, false>(mo, true);
         #pragma unroll 1
         for (; i < kmax; i++) run.template pair<BIG, true>(mo, i < np);
-        if (__any_sync(0xffffffffu, odd)) run.template single<BIG>(mo, (uint32_t)(s0 + 2ull * np), odd);
+        const uint32_t rmax = __reduce_max_sync(0xffffffffu, rem);
+        #pragma unroll 1
+        for (uint32_t r = 0; r < rmax; r++)
+            run.template single<BIG>(mo, (uint32_t)(s0 + (uint64_t)Run::K * np + r), r < rem);
         if (act) {
             const uint32_t c1 = mo.mul(run.a1, lane_coef(mo, tm, rho));          // fold a_j
             const uint32_t n1 = mo.mul2add<true>(C0, c1, C1, run.a0);            // eqnCombinePairs
@@ -288,8 +358,8 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
             if (big) lane2_item<LaneRun3, true>(mo, cg, valid, q, Q, rQ, C0, C1);
             else lane2_item<LaneRun3, false>(mo, cg, valid, q, Q, rQ, C0, C1);
         } else {
-            if (big) lane2_item<LaneRun2, true>(mo, cg, valid, q, Q, rQ, C0, C1);
-            else lane2_item<LaneRun2, false>(mo, cg, valid, q, Q, rQ, C0, C1);
+            if (big) lane2_item<LaneRun2Q, true>(mo, cg, valid, q, Q, rQ, C0, C1);
+            else lane2_item<LaneRun2Q, false>(mo, cg, valid, q, Q, rQ, C0, C1);
         }
         if (valid) partials[start[k] + q - part_base] = make_ulonglong2(C0, C1);
     }
