@@ -194,11 +194,15 @@ static const Variant kVariants[] = {
     {"c0 int s2/2 pairs", 0, residue_kernel<Mont32, 0, 0, 2, 2, true>, nullptr},
     {"c2 int s1/1 pairs", 2, residue_kernel<Mont64, 2, 0, 1, 1, true>, nullptr},
     {"c0 lane2", 0, nullptr, residue_lane2_kernel},                   // lane mode v2 (sorted lists)
+    // K-term FP64 steps for sum-aligned congruences (K for e = 2 / e = 3); measured on C4/C5 heads:
+    // 4/4 620/371 ms, 6/4 621/352, 6/5 583/342, 8/4 628/347, 8/5 594/337, 6/6 565/340 (term-by-term: 880/552)
+    {"c1 fp tuples 4/4", 1, residue_kernel<Mont64, 1, 1, 4, 4, true>, nullptr},
+    {"c1 fp tuples 6/6", 1, residue_kernel<Mont64, 1, 1, 6, 6, true>, nullptr},
 };
 static const int NVAR = sizeof kVariants / sizeof kVariants[0];
 static_assert(NVAR <= 32, "DevCtx::occ holds 32 variants");
-static const int kDefaultVariant[3] = {15, 6, 8};  // measured best (scripts/variant_sweep.py)
-static int g_variant[3] = {15, 6, 8};              // per class
+static const int kDefaultVariant[3] = {15, 17, 8};  // measured best (scripts/variant_sweep.py)
+static int g_variant[3] = {15, 17, 8};              // per class
 static const int kChunkFallback0 = 13;             // class-0 chunk variant when lane mode is unusable
 static void read_variant_env() {
     static bool done = false;

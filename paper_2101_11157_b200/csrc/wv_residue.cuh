@@ -439,6 +439,155 @@ struct RunD {
     }
 };
 
+// FP64 engine, K terms per step (sum-aligned chunks, 2^30 <= p < 2^44):
+//     1/u_0 + ... + 1/u_{K-1} = N / D,  u_i = (s+i)^E,
+//     D(s) = (s (s+1) ... (s+K-1))^E  (degree KE),   N(s) = sum_i prod_{j != i} u_j  (degree (K-1)E),
+// advanced by step-K forward differences held as exact integers in doubles.  Per step:
+// a1 <- a1 D + a0 N, a0 <- a0 D (3 exact EFT products, ModD) and (2K-1)E additions, against
+// K x (2 products + E additions) term by term.  Balanced values grow under the additions; every `rb`
+// steps all non-constant table entries are range-reduced, rb the largest with
+// p sum_{i <= KE} C(rb, i) <= 2^49 (then |D_0|, |N_0| <= 2^49 as ModD::mul needs, and every entry
+// stays an exact integer).
+template <int E, int K>
+struct RunDK {
+    static constexpr int DD = K * E, DN = (K - 1) * E;
+    double D[DD + 1], N[DN + 1], a0, a1;
+    __device__ __forceinline__ void setup(const ModD &md, uint64_t x) {     // x < p/2
+        const double s = (double)x;
+        double u, d1, d2;
+        if (E == 3) {
+            const double s2 = md.mul(s, s);
+            u = md.mul(s2, s);
+            d1 = md.reduce(__fma_rn(3.0, __dadd_rn(s2, s), 1.0));           // 3s^2 + 3s + 1
+            d2 = __fma_rn(6.0, s, 6.0);                                        // 6s + 6
+        } else {
+            u = md.mul(s, s);
+            d1 = __fma_rn(2.0, s, 1.0);
+            d2 = 2.0;
+        }
+        #pragma unroll
+        for (int i = 0; i <= DD; i++) {
+            double q[K], pre[K + 1], suf[K];
+            #pragma unroll
+            for (int k = 0; k < K; k++) {
+                q[k] = u;
+                u = md.reduce(__dadd_rn(u, d1));
+                d1 = __dadd_rn(d1, d2);
+                if (E == 3) { d1 = md.reduce(d1); d2 = __dadd_rn(d2, 6.0); }
+            }
+            pre[1] = q[0];
+            #pragma unroll
+            for (int k = 1; k < K; k++) pre[k + 1] = md.mul(pre[k], q[k]);
+            D[i] = pre[K];
+            if (i <= DN) {
+                suf[K - 1] = q[K - 1];
+                #pragma unroll
+                for (int k = K - 2; k >= 1; k--) suf[k] = md.mul(suf[k + 1], q[k]);
+                double n = suf[1];                                             // prod_{j != 0}
+                #pragma unroll
+                for (int k = 1; k < K - 1; k++) n = md.reduce(__dadd_rn(n, md.mul(pre[k], suf[k + 1])));
+                N[i] = md.reduce(__dadd_rn(n, pre[K - 1]));                    // prod_{j != K-1}
+            }
+        }
+        #pragma unroll
+        for (int k = 1; k <= DD; k++) {
+            #pragma unroll
+            for (int i = DD; i >= k; i--) D[i] = md.reduce(__dadd_rn(D[i], -D[i - 1]));
+        }
+        #pragma unroll
+        for (int k = 1; k <= DN; k++) {
+            #pragma unroll
+            for (int i = DN; i >= k; i--) N[i] = md.reduce(__dadd_rn(N[i], -N[i - 1]));
+        }
+        a0 = 1.0;
+        a1 = 0.0;
+    }
+    template <bool MASK>
+    __device__ __forceinline__ void step(const ModD &md, bool act) {
+        const double n1 = __dadd_rn(md.mul(a1, D[0]), md.mul(a0, N[0]));   // |a1| <= 2p
+        const double n0 = md.mul(a0, D[0]);
+        a1 = (!MASK || act) ? n1 : a1;
+        a0 = (!MASK || act) ? n0 : a0;
+        #pragma unroll
+        for (int i = 0; i < DD; i++) D[i] = __dadd_rn(D[i], D[i + 1]);
+        #pragma unroll
+        for (int i = 0; i < DN; i++) N[i] = __dadd_rn(N[i], N[i + 1]);
+    }
+    __device__ __forceinline__ void reduce(const ModD &md) {
+        #pragma unroll
+        for (int i = 0; i < DD; i++) D[i] = md.reduce(D[i]);
+        #pragma unroll
+        for (int i = 0; i < DN; i++) N[i] = md.reduce(N[i]);
+    }
+    // one term s = x, masked (u recomputed: masked steps advanced the tables of every lane)
+    __device__ __forceinline__ void single(const ModD &md, uint64_t x, bool act) {
+        const double s = (double)x;
+        const double w = E == 3 ? md.mul(md.mul(s, s), s) : md.mul(s, s);
+        const double n1 = __dadd_rn(md.mul(a1, w), a0);
+        const double n0 = md.mul(a0, w);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
+    }
+};
+
+// steps between range reductions of a RunDK table (see above), for the warp's largest p
+template <int DD>
+__device__ __forceinline__ uint32_t rundk_interval(uint64_t p) {
+    const double budget = 562949953421312.0 / (double)p;    // 2^49 / p
+    double c = 1.0, g = 1.0;                                 // C(r, i) running terms; g = sum_{i <= DD} C(r, i)
+    uint32_t r = 0;
+    for (;;) {                                               // g(r + 1) = sum_{i <= DD} C(r + 1, i)
+        const uint32_t rn = r + 1;
+        double gn = 0.0;
+        c = 1.0;
+        for (int i = 0; i <= DD && i <= (int)rn; i++) {
+            gn += c;
+            c = c * (double)(rn - i) / (double)(i + 1);
+        }
+        if (gn > budget || rn > 64) break;
+        r = rn;
+        g = gn;
+    }
+    (void)g;
+    return r ? r : 1;
+}
+
+template <class M, int E, int K>
+__device__ __forceinline__ void fp_tuple_work(const M &mo, const ModD &md, uint64_t p, uint64_t x0, uint64_t n,
+                                              typename M::W coef_m, typename M::W &C0, typename M::W &C1) {
+    using W = typename M::W;
+    const uint64_t ns = n / K, rem = n - K * ns;
+    const bool act = n != 0;
+    const uint64_t kmin = __reduce_min_sync(0xffffffffu, act ? (uint32_t)ns : 0xffffffffu);
+    if (kmin == 0xffffffffu) return;
+    const uint64_t kmax = __reduce_max_sync(0xffffffffu, act ? (uint32_t)ns : 0u);
+    const uint32_t rmax = __reduce_max_sync(0xffffffffu, (uint32_t)rem);
+    const uint32_t rb = __reduce_min_sync(0xffffffffu, rundk_interval<K * E>(p));
+    RunDK<E, K> run;
+    run.setup(md, act ? x0 : 1);
+    uint32_t since = 0;
+    uint64_t i = 0;
+    #pragma unroll 1
+    for (; i < kmin; i++) {
+        run.template step<false>(md, true);
+        if (++since == rb) { run.reduce(md); since = 0; }
+    }
+    #pragma unroll 1
+    for (; i < kmax; i++) {
+        run.template step<true>(md, i < ns);
+        if (++since == rb) { run.reduce(md); since = 0; }
+    }
+    for (uint32_t r = 0; r < rmax; r++) run.single(md, x0 + K * ns + r, r < rem);
+    if (act) {
+        W c0 = mo.mul((W)md.canon(run.a0), mo.r2);     // into the combine domain (Montgomery form)
+        W c1 = mo.mul((W)md.canon(run.a1), mo.r2);
+        c1 = mo.mul(c1, coef_m);                        // fold a_j
+        typename M::W n1 = mo.add(mo.mul(C0, c1), mo.mul(C1, c0));
+        C0 = mo.mul(C0, c0);
+        C1 = n1;
+    }
+}
+
 template <class M>
 __device__ __forceinline__ void combine(const M &mo, typename M::W &C0, typename M::W &C1,
                                         typename M::W c0, typename M::W c1) {
@@ -609,7 +758,7 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const War
 // minimum resident blocks per SM (caps registers): FP64 / 64-bit engines 3 (<= 80 regs: +2-3 % on
 // C4/C5 over 98 regs); the 32-bit IMAD engine is left unconstrained (a 64-register cap cost 8 % on C2)
 template <class M, int CLASS, int ENGINE, int S2, int S3, bool PAIRS = false>
-__global__ void __launch_bounds__(RES_THREADS, (ENGINE == 0 && CLASS == 0) ? 1 : 3)
+__global__ void __launch_bounds__(RES_THREADS, (ENGINE == 0 && CLASS == 0) ? 1 : ((ENGINE == 1 && PAIRS) ? 2 : 3))
 residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
                uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
                unsigned long long *__restrict__ counter, uint32_t class_mask,
@@ -718,7 +867,13 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
             if (lane == 0) tab.cont = 0;
             __syncwarp();
         }
-        if (ENGINE == 1) {
+        if (ENGINE == 1 && PAIRS && cg.seg) {                // four-term FP64 steps over the lane's run
+            md.init(r.p);
+            const uint64_t x0 = tab.first[0] + t0, nl = t1 > t0 ? t1 - t0 : 0;
+            // tuple widths: S2 / S3 reinterpreted as K for e = 2 / e = 3 (at least 2)
+            if (cg.e == 3) fp_tuple_work<M, 3, (S3 > 1 ? S3 : 2)>(mo, md, r.p, x0, nl, (W)tab.coef[0], C0, C1);
+            else fp_tuple_work<M, 2, (S2 > 1 ? S2 : 2)>(mo, md, r.p, x0, nl, (W)tab.coef[0], C0, C1);
+        } else if (ENGINE == 1) {
             md.init(r.p);
             if (cg.e == 3) {
                 if (prep) prepare_switch<M, RunD<M, 3>>(mo, md, tab, m);
