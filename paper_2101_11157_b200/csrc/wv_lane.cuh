@@ -27,18 +27,6 @@
 
 namespace wv {
 
-__constant__ const double2 *c_termr;     // {fl(1/xd), fl(1/yd)} per term (same index as c_terms)
-
-// floor(n / d) for n < 2^62, 0 < d < 2^32, rd = fl(1/d): double estimate (off by at most one for
-// quotients < 2^40), then an exact integer correction.
-__device__ __forceinline__ uint64_t fdiv(uint64_t n, uint32_t d, double rd) {
-    uint64_t q = (uint64_t)__dmul_rz(__ull2double_rz(n), rd);
-    const int64_t r = (int64_t)(n - q * d);
-    if (r < 0) q--;
-    else if (r >= (int64_t)d) q++;
-    return q;
-}
-
 // first s and count of x p < s < y p (strict) for p < 2^32: exact.
 __device__ __forceinline__ void lane_bounds(uint32_t p, const Term &t, double2 rr, uint64_t &first, uint32_t &cnt) {
     const uint64_t f = fdiv((uint64_t)t.xn * p, t.xd, rr.x) + 1;                  // floor(x p) + 1

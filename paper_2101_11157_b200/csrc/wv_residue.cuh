@@ -98,6 +98,27 @@ __host__ __device__ __forceinline__ int schedule(const Sched &s, uint64_t p, int
     return id;
 }
 
+__constant__ const double2 *c_termr;     // {fl(1/xd), fl(1/yd)} per term (same index as c_terms)
+
+// floor(n / d) for n < 2^62, 0 < d < 2^32, quotient < 2^40, rd = fl(1/d): double estimate (off by at
+// most one), then an exact integer correction.
+__device__ __forceinline__ uint64_t fdiv(uint64_t n, uint32_t d, double rd) {
+    uint64_t q = (uint64_t)__dmul_rz(__ull2double_rz(n), rd);
+    const int64_t r = (int64_t)(n - q * d);
+    if (r < 0) q--;
+    else if (r >= (int64_t)d) q++;
+    return q;
+}
+
+// first and count of integers s with x p < s < y p  (x = xn/xd, y = yn/yd), exact; p < 2^32
+// (xn p < 2^59), divisions by reciprocal estimate + correction
+__device__ __forceinline__ void sum_bounds_r(uint64_t p, const Term &t, double2 rr, uint64_t *first, uint64_t *count) {
+    const uint64_t f = fdiv((uint64_t)t.xn * p, t.xd, rr.x) + 1;                  // floor(x p) + 1
+    const uint64_t l = fdiv((uint64_t)t.yn * p + t.yd - 1, t.yd, rr.y) - 1;       // ceil(y p) - 1
+    *first = f;
+    *count = l >= f ? l - f + 1 : 0;
+}
+
 // first and count of integers s with x p < s < y p  (x = xn/xd, y = yn/yd), exact.
 __device__ __forceinline__ void sum_bounds(uint64_t p, const Term &t, uint64_t *first, uint64_t *count) {
     if (p < (1ull << 32)) {                 // 32-bit divisions; num * rem may exceed 32 bits
@@ -144,10 +165,18 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         }
         const Cong &c = c_cong[cid];
         uint64_t T = 0;
-        for (uint32_t j = 0; j < c.m; j++) {
-            uint64_t f, cnt;
-            sum_bounds(p, c_terms[c.off + j], &f, &cnt);
-            T += cnt;
+        if (p < (1ull << 32)) {
+            for (uint32_t j = 0; j < c.m; j++) {
+                uint64_t f, cnt;
+                sum_bounds_r(p, c_terms[c.off + j], c_termr[c.off + j], &f, &cnt);
+                T += cnt;
+            }
+        } else {
+            for (uint32_t j = 0; j < c.m; j++) {
+                uint64_t f, cnt;
+                sum_bounds(p, c_terms[c.off + j], &f, &cnt);
+                T += cnt;
+            }
         }
         uint64_t L = (T + 32ull * CAP_CHUNKS - 1) / (32ull * CAP_CHUNKS);
         if (L < LMIN) L = LMIN;
@@ -173,12 +202,17 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
             const uint64_t pl = primes[il];
             const int cl = schedule(sched, pl, (int)test);
             uint64_t Tl = 0;
-            if (cl >= 0 && cl < c_ncong)
+            if (lane_total && i != 32 * g) {
+                // lane mode v2: only the group's first record publishes the group's term count
+            } else if (il == i && cl == cid) {
+                Tl = T;                                          // this record is the group's last prime
+            } else if (cl >= 0 && cl < c_ncong) {
                 for (uint32_t jj = 0; jj < c_cong[cl].m; jj++) {
                     uint64_t f, cnt;
-                    sum_bounds(pl, c_terms[c_cong[cl].off + jj], &f, &cnt);
+                    sum_bounds_r(pl, c_terms[c_cong[cl].off + jj], c_termr[c_cong[cl].off + jj], &f, &cnt);
                     Tl += cnt;
                 }
+            }
             if (lane_total) {
                 // deferred: gq = the group's term count, converted to slices by lane_slices_kernel
                 nc = 1;

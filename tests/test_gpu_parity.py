@@ -304,6 +304,29 @@ def test_class2_64bit_montgomery_cross_congruence(wv):
     assert 0 <= out["BB1"][0] < p and 0 <= out["BB1"][1] < p
 
 
+def test_fp64_tuple_steps_near_class_top(wv):
+    """The FP64 engine's six-term steps range-reduce their difference tables every rb steps, rb the
+    largest with p sum_{i<=Ke} C(rb, i) <= 2^49: smallest just below 2^44.  Primes there (and a few
+    ragged ones at C4 size) must give the term-by-term FP64 variant's residues, and BIG-tier residues
+    must equal those of the paper's printed congruences BB30 / EE33 (non-sum-aligned, term by term)."""
+    ids = {name: vid for vid, name, cls in wv.kernel_variants()}
+    names = {c["name"]: c["id"] for c in wv.congruences()}
+    ps = [17592186044399, 17592186044297, 59000000023, 59000000149]   # < 2^44 (largest class-1 p); C4 size
+    try:
+        wv.set_kernel_variant(1, ids["c1 fp tuples 6/6"])
+        tw, tv = wv.residues_of(ps, 3)
+        wv.set_kernel_variant(1, ids["c1 fp s2/2"])
+        sw, sv = wv.residues_of(ps, 3)
+        assert tw.tolist() == sw.tolist() and tv.tolist() == sv.tolist()
+        wv.set_kernel_variant(1, -1)
+        wv.set_schedule_override(names["BB30"], names["EE33"])
+        pw, pv = wv.residues_of(ps[2:], 3)
+        assert pw.tolist() == tw[2:].tolist() and pv.tolist() == tv[2:].tolist()
+    finally:
+        wv.set_schedule_override(-1, -1)
+        wv.set_kernel_variant(1, -1)
+
+
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_c4_c5_sampled_primes(wv, name):
     """configs[3], configs[4]: the oracle's deterministic 8-prime samples of the full windows
