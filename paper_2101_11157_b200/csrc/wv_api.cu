@@ -248,18 +248,30 @@ static int ctx_get(DevCtx **out) {
             const int nc = (int)T.hdr.size();
             CK(cudaMemcpyToSymbol(c_cong, T.hdr.data(), T.hdr.size() * sizeof(Cong)));
             CK(cudaMemcpyToSymbol(c_ncong, &nc, sizeof nc));
+            // device copy: each congruence's sums sorted by left endpoint, bit 0 of pad set where the next
+            // interval starts where this one ends (x_{j+1} = y_j): consecutive integers, one run (wv_lane.cuh)
+            std::vector<Term> dev = T.terms;
+            for (const Cong &c : T.hdr) {
+                Term *b = dev.data() + c.off, *e = b + c.m;
+                std::sort(b, e, [](const Term &u, const Term &v) {
+                    return (unsigned __int128)u.xn * v.xd < (unsigned __int128)v.xn * u.xd;
+                });
+                for (Term *t = b; t < e; t++)
+                    t->pad = (t + 1 < e && (unsigned __int128)t->yn * t[1].xd == (unsigned __int128)t[1].xn * t->yd) ? 1u : 0u;
+            }
             Term *dt = nullptr;
-            CK(cudaMalloc(&dt, T.terms.size() * sizeof(Term)));
-            CK(cudaMemcpy(dt, T.terms.data(), T.terms.size() * sizeof(Term), cudaMemcpyHostToDevice));
+            CK(cudaMalloc(&dt, dev.size() * sizeof(Term)));
+            CK(cudaMemcpy(dt, dev.data(), dev.size() * sizeof(Term), cudaMemcpyHostToDevice));
             const Term *dtc = dt;
             CK(cudaMemcpyToSymbol(c_terms, &dtc, sizeof dtc));
-            std::vector<double2> rr(T.terms.size());          // reciprocals of the endpoint denominators
-            for (size_t i = 0; i < rr.size(); i++) rr[i] = make_double2(1.0 / T.terms[i].xd, 1.0 / T.terms[i].yd);
+            std::vector<double2> rr(dev.size());              // reciprocals of the endpoint denominators
+            for (size_t i = 0; i < rr.size(); i++) rr[i] = make_double2(1.0 / dev[i].xd, 1.0 / dev[i].yd);
             double2 *dr = nullptr;
             CK(cudaMalloc(&dr, rr.size() * sizeof(double2)));
             CK(cudaMemcpy(dr, rr.data(), rr.size() * sizeof(double2), cudaMemcpyHostToDevice));
             const double2 *drc = dr;
             CK(cudaMemcpyToSymbol(c_termr, &drc, sizeof drc));
+
         }
         for (int v = 0; v < NVAR; v++) {
             if (kVariants[v].fn)
@@ -610,6 +622,20 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         // per class: items [max(glo, gb[c]), min(ghi, gb[c+1])) of records [max(klo,kbd[c]), min(khi,kbd[c+1]));
         // unsorted input: every class kernel scans the whole batch and skips the other classes' records
         if (lane && h[3] > 0) {     // lane mode for class 0 (single batch guaranteed above)
+            {   // WV_LANE_CHAIN (benchmarking / tests): chain mode per exponent, default 1 (e = 2 only)
+                const char *ev = getenv("WV_LANE_CHAIN");
+                static uint32_t cur[64];
+                static bool init[64];
+                int dev = 0;
+                CK(cudaGetDevice(&dev));
+                const uint32_t cm = ev ? (uint32_t)strtoul(ev, nullptr, 0) : 1u;
+                if (dev >= 0 && dev < 64 && (!init[dev] || cur[dev] != cm)) {
+                    CK(cudaMemcpyToSymbolAsync(c_lane_chain, &cm, sizeof cm, 0, cudaMemcpyHostToDevice, st));
+                    CK(cudaStreamSynchronize(st));
+                    cur[dev] = cm;
+                    init[dev] = true;
+                }
+            }
             CK(cudaMemsetAsync(misc + M_CNT, 0, 8, st));
             EvPair ev{nullptr, nullptr, 0};
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }

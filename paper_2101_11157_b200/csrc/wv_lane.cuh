@@ -142,6 +142,26 @@ struct LaneRun2 {
         a1 = act ? n1 : a1;
         a0 = act ? n0 : a0;
     }
+    static __device__ __forceinline__ uint32_t term_w(const MontS &mo, uint32_t x) {   // x^2 R
+        const uint32_t xt = mo.mul(x, mo.r2);
+        return mo.mul(xt, xt);
+    }
+    // table + accumulators advance only where act (masked steps of chain mode keep tables aligned)
+    template <bool BIG>
+    __device__ __forceinline__ void pair_all(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        if (!act) *this = old;
+    }
+    // the table advances one step where act; the accumulators are left alone
+    template <bool BIG>
+    __device__ __forceinline__ void advance(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        a0 = old.a0;
+        a1 = old.a1;
+        if (!act) *this = old;
+    }
 };
 
 // e = 3 run: u = s^3 and its unit-step differences (3s^2+3s+1, 6s+6, 6), Montgomery form.
@@ -184,6 +204,26 @@ struct LaneRun3 {
         const uint32_t n0 = mo.mul(a0, w);
         a1 = act ? n1 : a1;
         a0 = act ? n0 : a0;
+    }
+    static __device__ __forceinline__ uint32_t term_w(const MontS &mo, uint32_t x) {   // x^3 R
+        const uint32_t xt = mo.mul(x, mo.r2);
+        return mo.mul(mo.mul(xt, xt), xt);
+    }
+    // table + accumulators advance only where act (masked steps of chain mode keep tables aligned)
+    template <bool BIG>
+    __device__ __forceinline__ void pair_all(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        if (!act) *this = old;
+    }
+    // the table advances one step where act; the accumulators are left alone
+    template <bool BIG>
+    __device__ __forceinline__ void advance(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        a0 = old.a0;
+        a1 = old.a1;
+        if (!act) *this = old;
     }
 };
 
@@ -250,6 +290,26 @@ struct LaneRun2Q {
         a1 = act ? n1 : a1;
         a0 = act ? n0 : a0;
     }
+    static __device__ __forceinline__ uint32_t term_w(const MontS &mo, uint32_t x) {   // x^2 R
+        const uint32_t xt = mo.mul(x, mo.r2);
+        return mo.mul(xt, xt);
+    }
+    // table + accumulators advance only where act (masked steps of chain mode keep tables aligned)
+    template <bool BIG>
+    __device__ __forceinline__ void pair_all(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        if (!act) *this = old;
+    }
+    // the table advances one step where act; the accumulators are left alone
+    template <bool BIG>
+    __device__ __forceinline__ void advance(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        a0 = old.a0;
+        a1 = old.a1;
+        if (!act) *this = old;
+    }
 };
 
 // One item: every sum of the lane's congruence, slice q of Q.  Returns the merged (C0, C1).
@@ -313,6 +373,129 @@ __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool
     }
 }
 
+
+__constant__ uint32_t c_lane_chain = 1u;   // chain mode per exponent (bit 0: e = 2, bit 1: e = 3); WV_LANE_CHAIN
+
+// Chain mode: the sums of a congruence sorted by left endpoint fall into chains of adjacent intervals
+// (x_{j+1} = y_j, flagged in Term.pad): their terms are consecutive integers, so one difference table
+// runs through the whole chain.  At a boundary inside a K-term step the lane finishes the sum with
+// its r = cnt mod K leftover terms and starts the next sum's accumulator with the other K - r terms
+// (single terms, u recomputed), then advances its table one step: no new set-up.  Per sum only the
+// bounds, the coefficient and the fold + merge remain.  (The generated congruences have 91 / 87 sums
+// in 47 / 24 chains (BG_SML / EG_SML), 3534 / 3535 in 1192 / 1065 (BG_BIG / EG_BIG).)
+// Every lane of the warp must have the same congruence (the caller checks).  Slices cut each chain's
+// integer range [F, E) into Q pieces.  A lane whose table does not sit at its next term (a sum that
+// is not contiguous for its p, or leftover terms without a straddle) triggers a set-up at each lane's
+// own position.
+template <class Run, bool BIG>
+__device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
+                                                 double rQ, uint32_t &C0, uint32_t &C1) {
+    constexpr uint32_t K = Run::K;
+    const uint32_t m = cg.m;
+    uint32_t rho[4];
+    rho[0] = mo.r2;
+    rho[1] = mo.mul(mo.r2, mo.r2);
+    rho[2] = mo.mul(rho[1], mo.r2);
+    rho[3] = mo.mul(rho[2], mo.r2);
+    uint32_t j = 0;
+    while (j < m) {
+        uint32_t je = j;
+        while (je + 1 < m && (c_terms[cg.off + je].pad & 1u)) je++;
+        uint64_t F = 1, E = 1;
+        if (valid) {
+            uint64_t f0, f1;
+            uint32_t n0, n1;
+            lane_bounds(mo.p, c_terms[cg.off + j], c_termr[cg.off + j], f0, n0);
+            lane_bounds(mo.p, c_terms[cg.off + je], c_termr[cg.off + je], f1, n1);
+            F = f0;
+            E = f1 + n1 > F ? f1 + n1 : F;
+        }
+        uint64_t lo = F, hi = E;
+        if (Q > 1) {
+            const uint64_t N = E - F;
+            lo = F + fdiv(N * q, (uint32_t)Q, rQ);
+            hi = F + fdiv(N * (q + 1), (uint32_t)Q, rQ);
+        }
+        if (!__any_sync(0xffffffffu, valid && lo < hi)) {
+            j = je + 1;
+            continue;
+        }
+        Run run;
+        run.setup(mo, (uint32_t)lo);
+        uint64_t t = lo, tp = lo;                     // next term; the term the table sits at
+        for (uint32_t jj = j; jj <= je; jj++) {
+            const Term tm = c_terms[cg.off + jj];
+            uint64_t f = 1;
+            uint32_t n = 0;
+            if (valid) lane_bounds(mo.p, tm, c_termr[cg.off + jj], f, n);
+            const uint64_t st = f > t ? f : t;
+            uint64_t v = f + n < hi ? f + n : hi;
+            if (v < st) v = st;
+            const bool has = valid && v > st;
+            if (__any_sync(0xffffffffu, has && st != tp)) {          // realign every lane's table at st
+                const uint32_t s0 = run.a0, s1 = run.a1;
+                run.setup(mo, (uint32_t)(valid ? st : 1));
+                run.a0 = s0;
+                run.a1 = s1;
+                tp = st;
+            }
+            t = st;
+            const uint32_t cnt = has ? (uint32_t)(v - t) : 0u;
+            const uint32_t ns = cnt / K, r = cnt - ns * K;
+            const uint32_t kmin = __reduce_min_sync(0xffffffffu, valid ? ns : 0xffffffffu);
+            const uint32_t kmax = __reduce_max_sync(0xffffffffu, valid ? ns : 0u);
+            uint32_t i = 0;
+            #pragma unroll 1
+            for (; i + 4 <= kmin; i += 4) {
+                run.template pair<BIG, false>(mo, true);
+                run.template pair<BIG, false>(mo, true);
+                run.template pair<BIG, false>(mo, true);
+                run.template pair<BIG, false>(mo, true);
+            }
+            #pragma unroll 1
+            for (; i < kmin; i++) run.template pair<BIG, false>(mo, true);
+            #pragma unroll 1
+            for (; i < kmax; i++) run.template pair_all<BIG>(mo, i < ns);
+            t += (uint64_t)K * ns;
+            tp += (uint64_t)K * ns;                    // the table moved only where it stepped (has => tp == t)
+            // straddle into the next sum of the chain when it continues at v with >= K - r terms
+            bool cont = false;
+            if (jj < je && valid && r > 0 && v == f + n) {
+                uint64_t fn;
+                uint32_t nn;
+                lane_bounds(mo.p, c_terms[cg.off + jj + 1], c_termr[cg.off + jj + 1], fn, nn);
+                const uint64_t vn = fn + nn < hi ? fn + nn : hi;
+                cont = fn == v && vn >= t + K;
+            }
+            uint32_t b0 = mo.r1, b1 = 0;
+            const bool anycont = __any_sync(0xffffffffu, cont);
+            const uint32_t nsingle = anycont ? K : __reduce_max_sync(0xffffffffu, r);
+            #pragma unroll 1
+            for (uint32_t k = 0; k < nsingle; k++) {
+                const bool inA = k < r, inB = cont && k >= r;
+                const uint32_t w = Run::term_w(mo, (uint32_t)(t + k));
+                const uint32_t s0 = inB ? b0 : run.a0, s1 = inB ? b1 : run.a1;
+                const uint32_t n1 = mo.mul2add<BIG>(s1, w, s0, mo.r1);
+                const uint32_t n0 = mo.mul(s0, w);
+                if (inB) { b0 = n0; b1 = n1; }
+                else if (inA) { run.a0 = n0; run.a1 = n1; }
+            }
+            if (anycont) run.template advance<BIG>(mo, cont);
+            if (cont) { t += K; tp = t; }
+            else t += r;                               // leftover singles: the table stays at tp
+            if (valid) {
+                const uint32_t c1 = mo.mul(run.a1, lane_coef(mo, tm, rho));          // fold a_j
+                const uint32_t m1 = mo.mul2add<true>(C0, c1, C1, run.a0);            // eqnCombinePairs
+                C0 = mo.mul(C0, run.a0);
+                C1 = m1;
+            }
+            run.a0 = cont ? b0 : mo.r1;
+            run.a1 = cont ? b1 : 0u;
+        }
+        j = je + 1;
+    }
+}
+
 // items it in [0, nitems) processed largest-first (groups ascend in p); gstart = exclusive scan of
 // gq (slices per group-test); start = per-record partial slots.
 __global__ void __launch_bounds__(RES_THREADS, 4)
@@ -320,6 +503,7 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
                      const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
                      uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
                      ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter) {
+    const uint32_t chain_mask = c_lane_chain;          // bit 0: chain mode for e = 2, bit 1: for e = 3
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned long long it = 0;
@@ -342,7 +526,21 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
         const double rQ = 1.0 / (double)Q;
         const uint32_t e = __reduce_max_sync(0xffffffffu, valid ? cg.e : 0u);   // one test per item
         const bool big = __any_sync(0xffffffffu, valid && r.p >= (1ull << 28));
-        if (e == 3) {
+        // chain mode when every valid lane has the same congruence (all but groups at a tier threshold)
+        const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+        const uint32_t cid0 = __shfl_sync(0xffffffffu, r.cid, vm ? __ffs(vm) - 1 : 0);
+        const bool chain = vm && __all_sync(0xffffffffu, !valid || r.cid == cid0) &&
+                           ((chain_mask >> (e == 3 ? 1 : 0)) & 1u);
+        if (chain) {
+            const Cong &cu = c_cong[cid0];
+            if (e == 3) {
+                if (big) lane2_chain_item<LaneRun3, true>(mo, cu, valid, q, Q, rQ, C0, C1);
+                else lane2_chain_item<LaneRun3, false>(mo, cu, valid, q, Q, rQ, C0, C1);
+            } else {
+                if (big) lane2_chain_item<LaneRun2Q, true>(mo, cu, valid, q, Q, rQ, C0, C1);
+                else lane2_chain_item<LaneRun2Q, false>(mo, cu, valid, q, Q, rQ, C0, C1);
+            }
+        } else if (e == 3) {
             if (big) lane2_item<LaneRun3, true>(mo, cg, valid, q, Q, rQ, C0, C1);
             else lane2_item<LaneRun3, false>(mo, cg, valid, q, Q, rQ, C0, C1);
         } else {

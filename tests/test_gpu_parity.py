@@ -287,6 +287,26 @@ def test_lane2_slicing_bit_exact(wv, items, monkeypatch):
         wv.set_kernel_variant(0, -1)
 
 
+@pytest.mark.parametrize("chain", ["0", "3"])
+def test_lane2_chain_modes_bit_exact(wv, chain, monkeypatch):
+    """Chain mode (one difference table through adjacent sums, straddling K-term steps) is on for e = 2 by
+    default; off for both exponents and on for both must give the same residues on windows where
+    sums are a few terms long (BB30 / EE33 just above 4096: empty, one- and two-term sums) and on a
+    C2-size window, and agree with the oracle."""
+    windows = [(4000, 9000, 3), (5, 300000, 3), ((1 << 24) - 4000, (1 << 24) + 4000, 3)]
+    for lo, hi, mode in windows:
+        _, ref = wv.search(lo, hi, mode)
+        monkeypatch.setenv("WV_LANE_CHAIN", chain)
+        _, got = wv.search(lo, hi, mode)
+        monkeypatch.delenv("WV_LANE_CHAIN")
+        assert got.tobytes() == ref.tobytes(), (lo, hi, chain)
+    ps = got["p"].tolist()
+    idx = sample_indices(len(ps), 32)
+    rw, rv = _oracle_arrays([ps[i] for i in idx], 3)
+    _assert_equal(got["p"][idx], got["res_w"][idx], rw, "W")
+    _assert_equal(got["p"][idx], got["res_v"][idx], rv, "V")
+
+
 def test_class2_64bit_montgomery_cross_congruence(wv):
     """p >= 2^44 runs the 64-bit Montgomery engine: two different congruences agree
     (BB1 vs BB30 for W, EE3 vs EE33 for V) on a prime just above 2^44 (property check)."""
