@@ -195,9 +195,11 @@ static const Variant kVariants[] = {
     {"c2 int s1/1 pairs", 2, residue_kernel<Mont64, 2, 0, 1, 1, true>, nullptr},
     {"c0 lane2", 0, nullptr, residue_lane2_kernel},                   // lane mode v2 (sorted lists)
     // K-term FP64 steps for sum-aligned congruences (K for e = 2 / e = 3); measured on C4/C5 heads:
-    // 4/4 620/371 ms, 6/4 621/352, 6/5 583/342, 8/4 628/347, 8/5 594/337, 6/6 565/340 (term-by-term: 880/552)
+    // 4/4 620/371 ms, 6/4 621/352, 6/5 583/342, 8/4 628/347, 8/5 594/337, 6/6 565/340, 8/6 560/334,
+    // 8/7 578/365, 10/6 560/379 (register spills beyond 6/6) (term-by-term: 880/552)
     {"c1 fp tuples 4/4", 1, residue_kernel<Mont64, 1, 1, 4, 4, true>, nullptr},
     {"c1 fp tuples 6/6", 1, residue_kernel<Mont64, 1, 1, 6, 6, true>, nullptr},
+
 };
 static const int NVAR = sizeof kVariants / sizeof kVariants[0];
 static_assert(NVAR <= 32, "DevCtx::occ holds 32 variants");
@@ -547,7 +549,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     double lane_items = 0;
     if (lane2) {
         const char *ev = getenv("WV_LANE_ITEMS");
-        lane_items = (ev ? atof(ev) : 4.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
+        lane_items = (ev ? atof(ev) : 3.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
     }
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
     uint64_t hs[4], ht[3];
