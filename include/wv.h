@@ -242,11 +242,18 @@ int wv_stats_reset(void);
 /* Residue-kernel variants (benchmarking / tests; process-global, not
  * thread-safe).  Primes fall in three classes: 0: p < 2^30 (32-bit
  * Montgomery), 1: 2^30 <= p < 2^44 (FP64 engine by default), 2: p >= 2^44
- * (64-bit Montgomery).  A variant fixes the engine (IMAD or FP64) and the
- * number of interleaved term streams per lane.  wv_kernel_variant_info
- * returns the name and class of variant id (WV_EINVAL past the end);
- * wv_set_kernel_variant selects it for its class (-1 restores the default).
- * Results are identical for every variant. */
+ * (64-bit Montgomery).  A variant fixes the kernel: for class 0 the lane-mode
+ * kernel ("c0 lane2", default; one prime per lane, sorted prime lists from the
+ * sieve) or a chunk kernel (engine, interleaved term streams per lane); for
+ * class 1 the K-term FP64 steps ("c1 fp tuples K2/K3", default 6/6) or the
+ * term-by-term FP64 / IMAD engines.  wv_kernel_variant_info returns the name
+ * and class of variant id (WV_EINVAL past the end); wv_set_kernel_variant
+ * selects it for its class (-1 restores the default).  Results are identical
+ * for every variant.  Environment knobs read per call (benchmarking only; the
+ * results never change): WV_VARIANT0/1/2 (default variant per class, read once),
+ * WV_LANE_ITEMS (lane-mode slices: items per resident warp, default 3),
+ * WV_LANE_CHAIN (lane-mode chain mode per exponent, bit 0: e = 2, bit 1: e = 3,
+ * default 1), WV_TH_<tier> (schedule threshold of a generated tier, read once). */
 int wv_kernel_variant_info(int id, char *name, size_t name_cap, int *cls);
 int wv_set_kernel_variant(int cls, int id);
 
