@@ -175,7 +175,7 @@ static int set_err(int code, const char *fmt, ...) {
 typedef void (*ResKern)(const Rec *, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, ulonglong2 *,
                         unsigned long long *, uint32_t, const uint32_t *, uint32_t);
 typedef void (*LaneKern)(const Rec *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
-                         uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *);
+                         uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *, unsigned long long *);
 struct Variant { const char *name; int cls; ResKern fn; LaneKern lane; };
 static const Variant kVariants[] = {
     {"c0 int s1/1", 0, residue_kernel<Mont32, 0, 0, 1, 1>, nullptr},
@@ -348,7 +348,8 @@ static const uint64_t PART_BUDGET = 1ull << 24;   // partial pairs per batch (25
 
 enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2 /* 2 slots: first k with p >= 2^30, >= 2^44 */,
        M_CNT = 4 /* 3 slots: work counters per class */, M_NHITS = 7, M_CHECKSUM = 8, M_NBASE1 = 9,
-       M_SPLIT = 10 /* 4 slots */, M_TERMS = 14 /* 3 slots: terms per class */, M_LANE_T = 17, M_SLOTS = 24 };
+       M_SPLIT = 10 /* 4 slots */, M_TERMS = 14 /* 3 slots: terms per class */, M_LANE_T = 17,
+       M_LANE_TERMS = 18 /* terms executed by the lane-mode v2 kernel (counted there) */, M_SLOTS = 24 };
 
 struct Layout {
     // problem
@@ -639,10 +640,12 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
                 }
             }
             CK(cudaMemsetAsync(misc + M_CNT, 0, 8, st));
+            CK(cudaMemsetAsync(misc + M_LANE_TERMS, 0, 8, st));
             EvPair ev{nullptr, nullptr, 0};
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
             LAUNCH(kVariants[var0].lane, c->sms * c->occ[var0], RES_THREADS, st, recs, start, gstart, gq, L.ngt, h[3],
-                   L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT));
+                   L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT),
+                   lane2 ? (unsigned long long *)(misc + M_LANE_TERMS) : nullptr);
             if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         for (int cls = 0; cls < 3; cls++) {
@@ -671,7 +674,14 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         LAUNCH(finalize_kernel, (unsigned)fb, 256, st, recs, start, klo, khi, glo, part, res_w, res_v);
     }
     if (stats && !evs.empty()) {
+        uint64_t lane_terms = 0;
+        if (lane && lane2) CK(cudaMemcpyAsync(&lane_terms, misc + M_LANE_TERMS, 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (lane_terms) {
+            std::lock_guard<std::mutex> lk(g_stats_mu);
+            g_stats.terms += lane_terms;
+            g_stats.terms32 += lane_terms;
+        }
         double ms = 0, ms32 = 0, msfp = 0;
         for (auto &e : evs) {
             float t = 0;

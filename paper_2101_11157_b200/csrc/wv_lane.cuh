@@ -315,7 +315,7 @@ struct LaneRun2Q {
 // One item: every sum of the lane's congruence, slice q of Q.  Returns the merged (C0, C1).
 template <class Run, bool BIG>
 __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
-                                           double rQ, uint32_t &C0, uint32_t &C1) {
+                                           double rQ, uint32_t &C0, uint32_t &C1, uint64_t &nterms) {
     const uint32_t m = valid ? cg.m : 0u;
     const uint32_t mmax = __reduce_max_sync(0xffffffffu, m);
     uint32_t rho[4];
@@ -341,6 +341,7 @@ __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool
             s0 = f + a;
         }
         const bool act = cnt != 0;
+        nterms += cnt;
         const uint32_t np = cnt / Run::K;                        // steps of K terms, then cnt % K singles
         const uint32_t kmin = __reduce_min_sync(0xffffffffu, act ? np : 0xffffffffu);
         if (kmin == 0xffffffffu) continue;                       // no lane has terms in this sum
@@ -389,7 +390,7 @@ __constant__ uint32_t c_lane_chain = 1u;   // chain mode per exponent (bit 0: e 
 // own position.
 template <class Run, bool BIG>
 __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
-                                                 double rQ, uint32_t &C0, uint32_t &C1) {
+                                                 double rQ, uint32_t &C0, uint32_t &C1, uint64_t &nterms) {
     constexpr uint32_t K = Run::K;
     const uint32_t m = cg.m;
     uint32_t rho[4];
@@ -481,6 +482,7 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
                 else if (inA) { run.a0 = n0; run.a1 = n1; }
             }
             if (anycont) run.template advance<BIG>(mo, cont);
+            nterms += cnt + (cont ? K - r : 0u);       // this sum's portion + the next sum's first K - r terms
             if (cont) { t += K; tp = t; }
             else t += r;                               // leftover singles: the table stays at tp
             if (valid) {
@@ -502,7 +504,8 @@ __global__ void __launch_bounds__(RES_THREADS, 4)
 residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                      const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
                      uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
-                     ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter) {
+                     ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
+                     unsigned long long *__restrict__ term_count) {
     const uint32_t chain_mask = c_lane_chain;          // bit 0: chain mode for e = 2, bit 1: for e = 3
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -526,6 +529,7 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
         const double rQ = 1.0 / (double)Q;
         const uint32_t e = __reduce_max_sync(0xffffffffu, valid ? cg.e : 0u);   // one test per item
         const bool big = __any_sync(0xffffffffu, valid && r.p >= (1ull << 28));
+        uint64_t nterms = 0;
         // chain mode when every valid lane has the same congruence (all but groups at a tier threshold)
         const uint32_t vm = __ballot_sync(0xffffffffu, valid);
         const uint32_t cid0 = __shfl_sync(0xffffffffu, r.cid, vm ? __ffs(vm) - 1 : 0);
@@ -534,20 +538,26 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
         if (chain) {
             const Cong &cu = c_cong[cid0];
             if (e == 3) {
-                if (big) lane2_chain_item<LaneRun3, true>(mo, cu, valid, q, Q, rQ, C0, C1);
-                else lane2_chain_item<LaneRun3, false>(mo, cu, valid, q, Q, rQ, C0, C1);
+                if (big) lane2_chain_item<LaneRun3, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                else lane2_chain_item<LaneRun3, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
             } else {
-                if (big) lane2_chain_item<LaneRun2Q, true>(mo, cu, valid, q, Q, rQ, C0, C1);
-                else lane2_chain_item<LaneRun2Q, false>(mo, cu, valid, q, Q, rQ, C0, C1);
+                if (big) lane2_chain_item<LaneRun2Q, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                else lane2_chain_item<LaneRun2Q, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
             }
         } else if (e == 3) {
-            if (big) lane2_item<LaneRun3, true>(mo, cg, valid, q, Q, rQ, C0, C1);
-            else lane2_item<LaneRun3, false>(mo, cg, valid, q, Q, rQ, C0, C1);
+            if (big) lane2_item<LaneRun3, true>(mo, cg, valid, q, Q, rQ, C0, C1, nterms);
+            else lane2_item<LaneRun3, false>(mo, cg, valid, q, Q, rQ, C0, C1, nterms);
         } else {
-            if (big) lane2_item<LaneRun2Q, true>(mo, cg, valid, q, Q, rQ, C0, C1);
-            else lane2_item<LaneRun2Q, false>(mo, cg, valid, q, Q, rQ, C0, C1);
+            if (big) lane2_item<LaneRun2Q, true>(mo, cg, valid, q, Q, rQ, C0, C1, nterms);
+            else lane2_item<LaneRun2Q, false>(mo, cg, valid, q, Q, rQ, C0, C1, nterms);
         }
         if (valid) partials[start[k] + q - part_base] = make_ulonglong2(C0, C1);
+        if (term_count) {                                   // executed terms (stats; the plan skips them)
+            uint64_t w = nterms;
+            #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            if (lane == 0) atomicAdd(term_count, (unsigned long long)w);
+        }
     }
 }
 

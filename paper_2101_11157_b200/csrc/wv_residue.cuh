@@ -164,8 +164,12 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
             nchunks[k] = 0; recs[k].T = 0; recs[k].p = 0; continue;
         }
         const Cong &c = c_cong[cid];
+        // lane mode v2 (class 0): the lane kernel counts its own terms and needs no chunking; only a
+        // group's first record computes the group's term count (below)
+        const bool lane2rec = lane_total && gq && p < WIDTH32_MAX;
         uint64_t T = 0;
-        if (p < (1ull << 32)) {
+        if (lane2rec) {
+        } else if (p < (1ull << 32)) {
             for (uint32_t j = 0; j < c.m; j++) {
                 uint64_t f, cnt;
                 sum_bounds_r(p, c_terms[c.off + j], c_termr[c.off + j], &f, &cnt);
@@ -182,7 +186,7 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         if (L < LMIN) L = LMIN;
         if (L > 0x40000000ull) L = 0x40000000ull;
         uint64_t nc = (T + 32 * L - 1) / (32 * L);
-        if (c.seg) {                                   // sum-aligned chunks: ceil(n_j / CT) per sum
+        if (c.seg && !lane2rec) {                      // sum-aligned chunks: ceil(n_j / CT) per sum
             // coarse index (when the stride holds it): segidx[k * segstride + r] = chunks of sums < 32 r
             const uint64_t CT = 32 * L;
             const bool idx = segidx && (c.m + 31) / 32 <= segstride;
@@ -204,7 +208,7 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
             uint64_t Tl = 0;
             if (lane_total && i != 32 * g) {
                 // lane mode v2: only the group's first record publishes the group's term count
-            } else if (il == i && cl == cid) {
+            } else if (il == i && cl == cid && !lane2rec) {
                 Tl = T;                                          // this record is the group's last prime
             } else if (cl >= 0 && cl < c_ncong) {
                 for (uint32_t jj = 0; jj < c_cong[cl].m; jj++) {
@@ -234,7 +238,7 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
         nchunks[k] = nc;
         if (p >= WIDTH32_MAX && nc > 0) atomicMin(first64, (unsigned long long)k);
         if (p >= FP64_MAX && nc > 0) atomicMin(first64 + 1, (unsigned long long)k);
-        atomicAdd(&terms[prime_class(p)], (unsigned long long)T);
+        if (!lane2rec) atomicAdd(&terms[prime_class(p)], (unsigned long long)T);
     }
     // lane-mode groups whose first prime is not class 0 (or beyond n) get Q = 0
     if (gq) {
@@ -1004,7 +1008,8 @@ __global__ void __launch_bounds__(RES_THREADS)
 residue_lane_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                     const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
                     uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
-                    ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter) {
+                    ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
+                    unsigned long long *__restrict__ /*term_count: the plan counts this kernel's terms*/) {
     using W = typename M::W;
     const int lane = threadIdx.x & 31;
     for (;;) {
