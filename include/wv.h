@@ -252,8 +252,8 @@ int wv_stats_reset(void);
  * for every variant.  Environment knobs read per call (benchmarking only; the
  * results never change): WV_VARIANT0/1/2 (default variant per class, read once),
  * WV_LANE_ITEMS (lane-mode slices: items per resident warp, default 3),
- * WV_LANE_CHAIN (lane-mode chain mode per exponent, bit 0: e = 2, bit 1: e = 3,
- * default 1), WV_TH_<tier> (schedule threshold of a generated tier, read once). */
+ * WV_LANE_CHAIN (lane-mode chain mode, bit 0: e = 2, bit 2: e = 3 with
+ * four-term steps (else pair steps per sum); default 5), WV_TH_<tier> (schedule threshold of a generated tier, read once). */
 int wv_kernel_variant_info(int id, char *name, size_t name_cap, int *cls);
 int wv_set_kernel_variant(int cls, int id);
 

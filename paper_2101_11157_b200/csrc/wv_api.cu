@@ -625,13 +625,13 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         // per class: items [max(glo, gb[c]), min(ghi, gb[c+1])) of records [max(klo,kbd[c]), min(khi,kbd[c+1]));
         // unsorted input: every class kernel scans the whole batch and skips the other classes' records
         if (lane && h[3] > 0) {     // lane mode for class 0 (single batch guaranteed above)
-            {   // WV_LANE_CHAIN (benchmarking / tests): chain mode per exponent, default 1 (e = 2 only)
+            {   // WV_LANE_CHAIN (benchmarking / tests): chain mode per exponent / W step width, default 5
                 const char *ev = getenv("WV_LANE_CHAIN");
                 static uint32_t cur[64];
                 static bool init[64];
                 int dev = 0;
                 CK(cudaGetDevice(&dev));
-                const uint32_t cm = ev ? (uint32_t)strtoul(ev, nullptr, 0) : 1u;
+                const uint32_t cm = ev ? (uint32_t)strtoul(ev, nullptr, 0) : 5u;
                 if (dev >= 0 && dev < 64 && (!init[dev] || cur[dev] != cm)) {
                     CK(cudaMemcpyToSymbolAsync(c_lane_chain, &cm, sizeof cm, 0, cudaMemcpyHostToDevice, st));
                     CK(cudaStreamSynchronize(st));

@@ -312,6 +312,108 @@ struct LaneRun2Q {
     }
 };
 
+// General K-term run for e = 2 or 3 (Montgomery form): D(s) = prod_{i<K} (s+i)^e (degree Ke) and
+// N(s) = sum_i prod_{j != i} (s+j)^e (degree (K-1)e), step-K forward differences.  The tables are set
+// up from D and N at Ke + 1 and (K-1)e + 1 points, each from K consecutive u = s^e (unit-step
+// differences) with prefix / suffix products.  LaneRun2Q is the hand-written e = 2, K = 4 case.
+template <int EE, int KK>
+struct LaneRunP {
+    static constexpr uint32_t K = KK;
+    static constexpr int DD = KK * EE, DN = (KK - 1) * EE;
+    uint32_t D[DD + 1], N[DN + 1], a0, a1;
+    __device__ __forceinline__ void setup(const MontS &mo, uint32_t x) {   // x < p
+        const uint32_t xt = mo.mul(x, mo.r2);
+        const uint32_t xx = mo.mul(xt, xt);
+        uint32_t u, d1, d2, d3 = 0;
+        if (EE == 3) {
+            const uint32_t r3 = mo.add(mo.add(mo.r1, mo.r1), mo.r1);
+            const uint32_t x3 = mo.add(mo.add(xt, xt), xt);
+            u = mo.mul(xx, xt);                                             // x^3
+            d1 = mo.add(mo.add(mo.add(xx, xx), xx), mo.add(x3, mo.r1));     // 3x^2 + 3x + 1
+            d3 = mo.add(r3, r3);                                            // 6
+            d2 = mo.add(mo.add(x3, x3), d3);                                // 6x + 6
+        } else {
+            u = xx;                                                         // x^2
+            d1 = mo.add(mo.add(xt, xt), mo.r1);                             // 2x + 1
+            d2 = mo.add(mo.r1, mo.r1);                                      // 2
+        }
+        #pragma unroll
+        for (int i = 0; i <= DD; i++) {
+            uint32_t q[KK], pre[KK + 1], suf[KK + 1];
+            #pragma unroll
+            for (int k = 0; k < KK; k++) {
+                q[k] = u;
+                u = mo.add(u, d1);
+                d1 = mo.add(d1, d2);
+                if (EE == 3) d2 = mo.add(d2, d3);
+            }
+            pre[1] = q[0];
+            #pragma unroll
+            for (int k = 1; k < KK; k++) pre[k + 1] = mo.mul(pre[k], q[k]);
+            D[i] = pre[KK];
+            if (i <= DN) {
+                suf[KK - 1] = q[KK - 1];
+                #pragma unroll
+                for (int k = KK - 2; k >= 1; k--) suf[k] = mo.mul(suf[k + 1], q[k]);
+                uint32_t n = mo.add(suf[1], pre[KK - 1]);                   // prod_{j != 0} + prod_{j != K-1}
+                #pragma unroll
+                for (int k = 1; k < KK - 1; k++) n = mo.add(n, mo.mul(pre[k], suf[k + 1]));
+                N[i] = n;
+            }
+        }
+        #pragma unroll
+        for (int k = 1; k <= DD; k++) {
+            #pragma unroll
+            for (int i = DD; i >= k; i--) D[i] = mo.sub(D[i], D[i - 1]);
+        }
+        #pragma unroll
+        for (int k = 1; k <= DN; k++) {
+            #pragma unroll
+            for (int i = DN; i >= k; i--) N[i] = mo.sub(N[i], N[i - 1]);
+        }
+        a0 = mo.r1;
+        a1 = 0;
+    }
+    template <bool BIG, bool MASK>
+    __device__ __forceinline__ void pair(const MontS &mo, bool act) {       // one step = K terms
+        const uint32_t n1 = mo.mul2add<BIG>(a1, D[0], a0, N[0]);
+        const uint32_t n0 = mo.mul(a0, D[0]);
+        a1 = (!MASK || act) ? n1 : a1;
+        a0 = (!MASK || act) ? n0 : a0;
+        #pragma unroll
+        for (int i = 0; i < DD; i++) D[i] = mo.add(D[i], D[i + 1]);
+        #pragma unroll
+        for (int i = 0; i < DN; i++) N[i] = mo.add(N[i], N[i + 1]);
+    }
+    static __device__ __forceinline__ uint32_t term_w(const MontS &mo, uint32_t x) {   // x^e R
+        const uint32_t xt = mo.mul(x, mo.r2);
+        const uint32_t x2 = mo.mul(xt, xt);
+        return EE == 3 ? mo.mul(x2, xt) : x2;
+    }
+    template <bool BIG>
+    __device__ __forceinline__ void single(const MontS &mo, uint32_t x, bool act) {
+        const uint32_t w = term_w(mo, x);
+        const uint32_t n1 = mo.mul2add<BIG>(a1, w, a0, mo.r1);
+        const uint32_t n0 = mo.mul(a0, w);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
+    }
+    template <bool BIG>
+    __device__ __forceinline__ void pair_all(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        if (!act) *this = old;
+    }
+    template <bool BIG>
+    __device__ __forceinline__ void advance(const MontS &mo, bool act) {
+        const auto old = *this;
+        pair<BIG, false>(mo, true);
+        a0 = old.a0;
+        a1 = old.a1;
+        if (!act) *this = old;
+    }
+};
+
 // One item: every sum of the lane's congruence, slice q of Q.  Returns the merged (C0, C1).
 template <class Run, bool BIG>
 __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
@@ -375,7 +477,8 @@ __device__ __forceinline__ void lane2_item(const MontS &mo, const Cong &cg, bool
 }
 
 
-__constant__ uint32_t c_lane_chain = 1u;   // chain mode per exponent (bit 0: e = 2, bit 1: e = 3); WV_LANE_CHAIN
+__constant__ uint32_t c_lane_chain = 5u;   // bit 0: chain mode for e = 2; bit 2: chain mode with four-term steps
+                                           // for e = 3 (else pair steps per sum) (WV_LANE_CHAIN)
 
 // Chain mode: the sums of a congruence sorted by left endpoint fall into chains of adjacent intervals
 // (x_{j+1} = y_j, flagged in Term.pad): their terms are consecutive integers, so one difference table
@@ -534,12 +637,14 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
         const uint32_t vm = __ballot_sync(0xffffffffu, valid);
         const uint32_t cid0 = __shfl_sync(0xffffffffu, r.cid, vm ? __ffs(vm) - 1 : 0);
         const bool chain = vm && __all_sync(0xffffffffu, !valid || r.cid == cid0) &&
-                           ((chain_mask >> (e == 3 ? 1 : 0)) & 1u);
+                           ((chain_mask >> (e == 3 ? 2 : 0)) & 1u);
         if (chain) {
             const Cong &cu = c_cong[cid0];
-            if (e == 3) {
-                if (big) lane2_chain_item<LaneRun3, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
-                else lane2_chain_item<LaneRun3, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+            // (six-term steps, LaneRunP<3, 6> / <2, 6>, measured slower: C2 residue 17.3 / 15.7 ms vs 13.1)
+            // (chains with W pair steps measured slower than without: C2 residue 13.64 vs 13.29 ms; no longer built)
+            if (e == 3) {                                  // four-term W steps
+                if (big) lane2_chain_item<LaneRunP<3, 4>, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                else lane2_chain_item<LaneRunP<3, 4>, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
             } else {
                 if (big) lane2_chain_item<LaneRun2Q, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
                 else lane2_chain_item<LaneRun2Q, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);

@@ -287,10 +287,11 @@ def test_lane2_slicing_bit_exact(wv, items, monkeypatch):
         wv.set_kernel_variant(0, -1)
 
 
-@pytest.mark.parametrize("chain", ["0", "3"])
+@pytest.mark.parametrize("chain", ["0", "1", "4"])
 def test_lane2_chain_modes_bit_exact(wv, chain, monkeypatch):
-    """Chain mode (one difference table through adjacent sums, straddling K-term steps) is on for e = 2 by
-    default; off for both exponents and on for both must give the same residues on windows where
+    """Chain mode (one difference table through adjacent sums, straddling K-term steps) is on by default
+    (e = 2 and e = 3 four-term steps: WV_LANE_CHAIN = 5); no chains with W pair steps (0), e = 2 only (1)
+    and e = 3 only (4) must give the same residues on windows where
     sums are a few terms long (BB30 / EE33 just above 4096: empty, one- and two-term sums) and on a
     C2-size window, and agree with the oracle."""
     windows = [(4000, 9000, 3), (5, 300000, 3), ((1 << 24) - 4000, (1 << 24) + 4000, 3)]
