@@ -251,7 +251,7 @@ int wv_stats_reset(void);
  * selects it for its class (-1 restores the default).  Results are identical
  * for every variant.  Environment knobs read per call (benchmarking only; the
  * results never change): WV_VARIANT0/1/2 (default variant per class, read once),
- * WV_LANE_ITEMS (lane-mode slices: items per resident warp, default 3),
+ * WV_LANE_ITEMS (lane-mode slices: items per resident warp, default 2),
  * WV_LANE_CHAIN (lane-mode chain mode, bit 0: e = 2, bit 2: e = 3 with
  * four-term steps (else pair steps per sum); default 5), WV_TH_<tier> (schedule threshold of a generated tier, read once). */
 int wv_kernel_variant_info(int id, char *name, size_t name_cap, int *cls);

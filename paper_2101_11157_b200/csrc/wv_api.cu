@@ -550,7 +550,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     double lane_items = 0;
     if (lane2) {
         const char *ev = getenv("WV_LANE_ITEMS");
-        lane_items = (ev ? atof(ev) : 3.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
+        lane_items = (ev ? atof(ev) : 2.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
     }
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
     uint64_t hs[4], ht[3];
