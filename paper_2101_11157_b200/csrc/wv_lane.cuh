@@ -506,12 +506,14 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
         uint32_t je = j;
         while (je + 1 < m && (c_terms[cg.off + je].pad & 1u)) je++;
         uint64_t F = 1, E = 1;
+        uint64_t fc = 1;                              // bounds of the chain's current sum (computed once)
+        uint32_t nc = 0;
         if (valid) {
-            uint64_t f0, f1;
-            uint32_t n0, n1;
-            lane_bounds(mo.p, c_terms[cg.off + j], c_termr[cg.off + j], f0, n0);
+            uint64_t f1;
+            uint32_t n1;
+            lane_bounds(mo.p, c_terms[cg.off + j], c_termr[cg.off + j], fc, nc);
             lane_bounds(mo.p, c_terms[cg.off + je], c_termr[cg.off + je], f1, n1);
-            F = f0;
+            F = fc;
             E = f1 + n1 > F ? f1 + n1 : F;
         }
         uint64_t lo = F, hi = E;
@@ -528,10 +530,13 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
         run.setup(mo, (uint32_t)lo);
         uint64_t t = lo, tp = lo;                     // next term; the term the table sits at
         for (uint32_t jj = j; jj <= je; jj++) {
-            const Term tm = c_terms[cg.off + jj];
-            uint64_t f = 1;
-            uint32_t n = 0;
-            if (valid) lane_bounds(mo.p, tm, c_termr[cg.off + jj], f, n);
+            const uint64_t f = fc;
+            const uint32_t n = nc;
+            uint64_t fn = 1;                          // the next sum's bounds (also used for the straddle)
+            uint32_t nn = 0;
+            if (jj < je && valid) lane_bounds(mo.p, c_terms[cg.off + jj + 1], c_termr[cg.off + jj + 1], fn, nn);
+            fc = fn;
+            nc = nn;
             const uint64_t st = f > t ? f : t;
             uint64_t v = f + n < hi ? f + n : hi;
             if (v < st) v = st;
@@ -565,9 +570,6 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             // straddle into the next sum of the chain when it continues at v with >= K - r terms
             bool cont = false;
             if (jj < je && valid && r > 0 && v == f + n) {
-                uint64_t fn;
-                uint32_t nn;
-                lane_bounds(mo.p, c_terms[cg.off + jj + 1], c_termr[cg.off + jj + 1], fn, nn);
                 const uint64_t vn = fn + nn < hi ? fn + nn : hi;
                 cont = fn == v && vn >= t + K;
             }
@@ -589,8 +591,8 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             if (cont) { t += K; tp = t; }
             else t += r;                               // leftover singles: the table stays at tp
             if (valid) {
-                const uint32_t c1 = mo.mul(run.a1, lane_coef(mo, tm, rho));          // fold a_j
-                const uint32_t m1 = mo.mul2add<true>(C0, c1, C1, run.a0);            // eqnCombinePairs
+                const uint32_t c1 = mo.mul(run.a1, lane_coef(mo, c_terms[cg.off + jj], rho));   // fold a_j
+                const uint32_t m1 = mo.mul2add<true>(C0, c1, C1, run.a0);                   // eqnCombinePairs
                 C0 = mo.mul(C0, run.a0);
                 C1 = m1;
             }
