@@ -1,25 +1,25 @@
 // wv_lane.cuh -- class-0 lane-mode residue kernel (sorted prime lists, 5 <= p < 2^30).
 //
 // A warp item is (group of 32 consecutive primes of one test, slice q of Q).  Lane l owns
-// record (32 g + l, test) and walks every sum j of its congruence,
-// taking slice q of each: for a sum with n_j terms, [floor(q n_j / Q), floor((q+1) n_j / Q)).
-// Neighbouring primes share the congruence and have nearly equal n_j, so all lanes cross sum
-// boundaries together: per sum one unmasked loop of min-count pair steps, then a short masked
-// tail.  (The chunk kernel splits one record over 64 lane streams instead; with C2-size primes
-// and ~90-sum congruences its streams cross sum boundaries at different times and the lockstep
-// loop breaks every ~8 terms.)
+// record (32 g + l, test) and walks every sum j of its congruence.
+// Neighbouring primes share the congruence and have nearly equal term counts, so all lanes cross
+// sum boundaries together: per sum one unmasked loop of min-count steps, then a short masked tail.
+// (The chunk kernel splits one record over 64 lane streams instead; with C2-size primes and ~90-sum
+// congruences its streams cross sum boundaries at different times and the lockstep loop breaks
+// every ~8 terms.)
 //
 // Arithmetic: everything in Montgomery form x R mod p (R = 2^32), lazy in [0, 2p), with the
 // subtractive REDC  m = T_lo p^{-1} mod R,  REDC(T) = T_hi - hi(m p) + p  -- the low words cancel
 // exactly, so no carry is propagated -- which lies in (0, p + T_hi].
 //
-// The sum of inverses is the ratio a1/a0 of eqnComputeS, advanced two terms at a time:
-//     1/u1 + 1/u2 = N / D,   D = u1 u2,  N = u1 + u2,
+// The sum of inverses is the ratio a1/a0 of eqnComputeS, advanced K terms at a time:
+//     1/u_0 + ... + 1/u_{K-1} = N / D,   D = prod u_i,  N = sum_i prod_{j != i} u_j,  u_i = (s+i)^e,
 //     a1 <- REDC(a1 D + a0 N),   a0 <- REDC(a0 D)          (ratio += N/D; one REDC for both products)
-// e = 2 (V): D(s) = (s (s+1))^2 and N(s) = s^2 + (s+1)^2 are polynomials in s of degree 4 and 2;
-//            step-2 forward differences advance them with modular adds only: 2 products per pair.
-// e = 3 (W): u = s^3 by unit-step finite differences, D = u1 u2 (one product), N = u1 + u2:
-//            3 products per pair (the degree-6 difference table costs more adds than it saves).
+// D(s), N(s) are polynomials in s (degree Ke, (K-1)e) advanced by step-K forward differences with
+// modular adds only.  K = 4 for both tests (LaneRun2Q, LaneRunP<3,4>); the pair step with
+// u = s^3 by unit differences (LaneRun3) serves e = 3 outside chain mode.
+// Chain mode (lane2_chain_item): the sums, sorted by left endpoint, form chains of adjacent
+// intervals whose terms are consecutive integers, so one table runs through a chain.
 // At the end of a sum: c1 <- a_j c1 (fold) and (C0, C1) (+) (c0, c1) (eqnCombinePairs).
 #pragma once
 #include <stdint.h>
@@ -87,82 +87,6 @@ __device__ __forceinline__ uint32_t lane_coef(const MontS &mo, const Term &t, co
     if (t.neg) a = mo.sub(0u, a);
     return a;
 }
-
-// e = 2 run: D, its three leading step-2 differences and the constant fourth; N, its first
-// difference and the constant second -- all in Montgomery form.
-struct LaneRun2 {
-    static constexpr uint32_t K = 2;                  // terms per step
-    uint32_t D0, D1, D2, D3, Dc, N0, N1, Nc, a0, a1;
-    __device__ __forceinline__ void setup(const MontS &mo, uint32_t x) {   // x < p
-        const uint32_t xt = mo.mul(x, mo.r2);                               // x R
-        const uint32_t r2_ = mo.add(mo.r1, mo.r1), r4 = mo.add(r2_, r2_), r6 = mo.add(r4, r2_), r8 = mo.add(r4, r4);
-        const uint32_t x2t = mo.add(xt, xt), x4t = mo.add(x2t, x2t), x8t = mo.add(x4t, x4t);
-        uint32_t t = mo.mul(xt, mo.add(xt, mo.r1));                         // x (x+1) R
-        uint32_t g = mo.add(x4t, r6);                                       // t(x+2) - t(x) = 4x + 6
-        uint32_t v[5];
-        #pragma unroll
-        for (int i = 0; i < 5; i++) {
-            v[i] = mo.mul(t, t);                                            // (x_i (x_i + 1))^2 R, x_i = x + 2i
-            t = mo.add(t, g);
-            g = mo.add(g, r8);
-        }
-        #pragma unroll
-        for (int k = 1; k < 5; k++) {
-            #pragma unroll
-            for (int i = 4; i >= k; i--) v[i] = mo.sub(v[i], v[i - 1]);
-        }
-        D0 = v[0]; D1 = v[1]; D2 = v[2]; D3 = v[3]; Dc = v[4];
-        const uint32_t xx = mo.mul(xt, xt);                                 // x^2 R
-        N0 = mo.add(mo.add(xx, xx), mo.add(x2t, mo.r1));                    // 2x^2 + 2x + 1
-        N1 = mo.add(x8t, mo.add(r8, r4));                                   // 8x + 12
-        Nc = mo.add(r8, r8);                                                // 16
-        a0 = mo.r1;
-        a1 = 0;
-    }
-    template <bool BIG, bool MASK>
-    __device__ __forceinline__ void pair(const MontS &mo, bool act) {
-        const uint32_t n1 = mo.mul2add<BIG>(a1, D0, a0, N0);
-        const uint32_t n0 = mo.mul(a0, D0);
-        a1 = (!MASK || act) ? n1 : a1;
-        a0 = (!MASK || act) ? n0 : a0;
-        D0 = mo.add(D0, D1);
-        D1 = mo.add(D1, D2);
-        D2 = mo.add(D2, D3);
-        D3 = mo.add(D3, Dc);
-        N0 = mo.add(N0, N1);
-        N1 = mo.add(N1, Nc);
-    }
-    // one term s = x (x < p), masked
-    template <bool BIG>
-    __device__ __forceinline__ void single(const MontS &mo, uint32_t x, bool act) {
-        const uint32_t xt = mo.mul(x, mo.r2);
-        const uint32_t u = mo.mul(xt, xt);
-        const uint32_t n1 = mo.mul2add<BIG>(a1, u, a0, mo.r1);
-        const uint32_t n0 = mo.mul(a0, u);
-        a1 = act ? n1 : a1;
-        a0 = act ? n0 : a0;
-    }
-    static __device__ __forceinline__ uint32_t term_w(const MontS &mo, uint32_t x) {   // x^2 R
-        const uint32_t xt = mo.mul(x, mo.r2);
-        return mo.mul(xt, xt);
-    }
-    // table + accumulators advance only where act (masked steps of chain mode keep tables aligned)
-    template <bool BIG>
-    __device__ __forceinline__ void pair_all(const MontS &mo, bool act) {
-        const auto old = *this;
-        pair<BIG, false>(mo, true);
-        if (!act) *this = old;
-    }
-    // the table advances one step where act; the accumulators are left alone
-    template <bool BIG>
-    __device__ __forceinline__ void advance(const MontS &mo, bool act) {
-        const auto old = *this;
-        pair<BIG, false>(mo, true);
-        a0 = old.a0;
-        a1 = old.a1;
-        if (!act) *this = old;
-    }
-};
 
 // e = 3 run: u = s^3 and its unit-step differences (3s^2+3s+1, 6s+6, 6), Montgomery form.
 struct LaneRun3 {
