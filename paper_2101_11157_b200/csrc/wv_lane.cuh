@@ -23,6 +23,7 @@
 // At the end of a sum: c1 <- a_j c1 (fold) and (C0, C1) (+) (c0, c1) (eqnCombinePairs).
 #pragma once
 #include <stdint.h>
+#include <type_traits>
 #include "wv_residue.cuh"
 
 namespace wv {
@@ -529,7 +530,23 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
 
 // items it in [0, nitems) processed largest-first (groups ascend in p); gstart = exclusive scan of
 // gq (slices per group-test); start = per-record partial slots.
-__global__ void __launch_bounds__(RES_THREADS, 4)
+// Step widths in chain mode (terms per step) for W (e = 3) and V (e = 2); build-time choices.
+#ifndef WV_LANE_KW
+#define WV_LANE_KW 4
+#endif
+#ifndef WV_LANE_KV
+#define WV_LANE_KV 4
+#endif
+using RunW = LaneRunP<3, WV_LANE_KW>;
+using RunV = std::conditional<WV_LANE_KV == 4, LaneRun2Q, LaneRunP<2, WV_LANE_KV>>::type;   // K = 4: hand-written
+
+// Resident blocks per SM the register allocation targets: 2 (up to 128 registers, 16 warps/SM).
+// Measured on C2 (residue ms): 4 blocks (64 registers, spills in the per-sum code) 12.18, 3: 11.59,
+// 2: 11.13, 1: 11.05; 2 keeps more warps for small windows.
+#ifndef WV_LANE2_MINB
+#define WV_LANE2_MINB 2
+#endif
+__global__ void __launch_bounds__(RES_THREADS, WV_LANE2_MINB)
 residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                      const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
                      uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
@@ -569,11 +586,11 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
             // (six-term steps, LaneRunP<3, 6> / <2, 6>, measured slower: C2 residue 17.3 / 15.7 ms vs 13.1)
             // (chains with W pair steps measured slower than without: C2 residue 13.64 vs 13.29 ms; no longer built)
             if (e == 3) {                                  // four-term W steps
-                if (big) lane2_chain_item<LaneRunP<3, 4>, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
-                else lane2_chain_item<LaneRunP<3, 4>, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                if (big) lane2_chain_item<RunW, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                else lane2_chain_item<RunW, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
             } else {
-                if (big) lane2_chain_item<LaneRun2Q, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
-                else lane2_chain_item<LaneRun2Q, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                if (big) lane2_chain_item<RunV, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                else lane2_chain_item<RunV, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
             }
         } else if (e == 3) {
             if (big) lane2_item<LaneRun3, true>(mo, cg, valid, q, Q, rQ, C0, C1, nterms);
