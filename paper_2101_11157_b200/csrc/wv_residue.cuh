@@ -796,7 +796,10 @@ __device__ __forceinline__ void lane_work(const M &mo, const ModD &md, const War
 // minimum resident blocks per SM (caps registers): FP64 / 64-bit engines 3 (<= 80 regs: +2-3 % on
 // C4/C5 over 98 regs); the 32-bit IMAD engine is left unconstrained (a 64-register cap cost 8 % on C2)
 template <class M, int CLASS, int ENGINE, int S2, int S3, bool PAIRS = false>
-__global__ void __launch_bounds__(RES_THREADS, (ENGINE == 0 && CLASS == 0) ? 1 : ((ENGINE == 1 && PAIRS) ? 2 : 3))
+#ifndef WV_FPT_MINB
+#define WV_FPT_MINB 2       // FP64 K-term kernels: resident blocks per SM targeted by register allocation
+#endif
+__global__ void __launch_bounds__(RES_THREADS, (ENGINE == 0 && CLASS == 0) ? 1 : ((ENGINE == 1 && PAIRS) ? WV_FPT_MINB : 3))
 residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
                uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
                unsigned long long *__restrict__ counter, uint32_t class_mask,
