@@ -406,16 +406,21 @@ __constant__ uint32_t c_lane_chain = 5u;   // bit 0: chain mode for e = 2; bit 2
                                            // for e = 3 (else pair steps per sum) (WV_LANE_CHAIN)
 
 // Chain mode: the sums of a congruence sorted by left endpoint fall into chains of adjacent intervals
-// (x_{j+1} = y_j, flagged in Term.pad): their terms are consecutive integers, so one difference table
-// runs through the whole chain.  At a boundary inside a K-term step the lane finishes the sum with
-// its r = cnt mod K leftover terms and starts the next sum's accumulator with the other K - r terms
-// (single terms, u recomputed), then advances its table one step: no new set-up.  Per sum only the
-// bounds, the coefficient and the fold + merge remain.  (The generated congruences have 91 / 87 sums
+// (x_{j+1} = y_j, flagged in Term.pad): for p >= 7 their terms are consecutive integers (R5), so one
+// difference table and ONE accumulator run through the whole chain, and the sums are separated by
+// summation by parts (Abel):  with P_j the running sum of s^-e through the end of sum j,
+//     sum_j a_j S_j = a_J P_J - sum_{j < J} (a_{j+1} - a_j) P_j .
+// At the end of sum j the lane takes a snapshot P_j = the accumulator plus the r < K terms of sum j
+// that do not fill a whole K-term step (single terms, u recomputed, on a copy), folds it with
+// a_j - a_{j+1} (a_J for the last sum) and merges it into (C0, C1); the r terms stay pending and
+// enter the accumulator with the next step.  Per sum: bounds, coefficient, < K singles, one fold +
+// merge -- no table set-up and no accumulator restart.  (The generated congruences have 91 / 87 sums
 // in 47 / 24 chains (BG_SML / EG_SML), 3534 / 3535 in 1192 / 1065 (BG_BIG / EG_BIG).)
 // Every lane of the warp must have the same congruence (the caller checks).  Slices cut each chain's
-// integer range [F, E) into Q pieces.  A lane whose table does not sit at its next term (a sum that
-// is not contiguous for its p, or leftover terms without a straddle) triggers a set-up at each lane's
-// own position.
+// integer range [F, E) into Q pieces (prefix sums over the slice's terms; the identity holds for any
+// P sequence).  A lane whose next sum does not start where its previous one ended (p < 7, R5) absorbs
+// its pending terms and realigns its table there; a realignment sets up every lane's table at its
+// own position (accumulators kept).
 template <class Run, bool BIG>
 __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
                                                  double rQ, uint32_t &C0, uint32_t &C1, uint64_t &nterms) {
@@ -453,28 +458,27 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
         }
         Run run;
         run.setup(mo, (uint32_t)lo);
-        uint64_t t = lo, tp = lo;                     // next term; the term the table sits at
+        uint64_t t = lo, tp = lo;                     // accumulator covers [lo, t); the table sits at tp
+        uint32_t coef = valid ? lane_coef(mo, c_terms[cg.off + j], rho) : 0u;
         for (uint32_t jj = j; jj <= je; jj++) {
             const uint64_t f = fc;
             const uint32_t n = nc;
-            uint64_t fn = 1;                          // the next sum's bounds (also used for the straddle)
-            uint32_t nn = 0;
-            if (jj < je && valid) lane_bounds(mo.p, c_terms[cg.off + jj + 1], c_termr[cg.off + jj + 1], fn, nn);
-            fc = fn;
-            nc = nn;
-            const uint64_t st = f > t ? f : t;
-            uint64_t v = f + n < hi ? f + n : hi;
-            if (v < st) v = st;
-            const bool has = valid && v > st;
-            if (__any_sync(0xffffffffu, has && st != tp)) {          // realign every lane's table at st
+            uint32_t coef_n = 0;
+            if (jj < je && valid) {
+                lane_bounds(mo.p, c_terms[cg.off + jj + 1], c_termr[cg.off + jj + 1], fc, nc);
+                coef_n = lane_coef(mo, c_terms[cg.off + jj + 1], rho);
+            }
+            if (__any_sync(0xffffffffu, valid && t != tp)) {          // realign every lane's table at t
                 const uint32_t s0 = run.a0, s1 = run.a1;
-                run.setup(mo, (uint32_t)(valid ? st : 1));
+                run.setup(mo, (uint32_t)(valid ? t : 1));
                 run.a0 = s0;
                 run.a1 = s1;
-                tp = st;
+                tp = t;
             }
-            t = st;
-            const uint32_t cnt = has ? (uint32_t)(v - t) : 0u;
+            // this sum's end within the slice; steps of K while they fit, r < K terms left over
+            uint64_t b = f + n < hi ? f + n : hi;
+            if (b < t) b = t;
+            const uint32_t cnt = valid ? (uint32_t)(b - t) : 0u;
             const uint32_t ns = cnt / K, r = cnt - ns * K;
             const uint32_t kmin = __reduce_min_sync(0xffffffffu, valid ? ns : 0xffffffffu);
             const uint32_t kmax = __reduce_max_sync(0xffffffffu, valid ? ns : 0u);
@@ -491,38 +495,41 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             #pragma unroll 1
             for (; i < kmax; i++) run.template pair_all<BIG>(mo, i < ns);
             t += (uint64_t)K * ns;
-            tp += (uint64_t)K * ns;                    // the table moved only where it stepped (has => tp == t)
-            // straddle into the next sum of the chain when it continues at v with >= K - r terms
-            bool cont = false;
-            if (jj < je && valid && r > 0 && v == f + n) {
-                const uint64_t vn = fn + nn < hi ? fn + nn : hi;
-                cont = fn == v && vn >= t + K;
-            }
-            uint32_t b0 = mo.r1, b1 = 0;
-            const bool anycont = __any_sync(0xffffffffu, cont);
-            const uint32_t nsingle = anycont ? K : __reduce_max_sync(0xffffffffu, r);
+            tp += (uint64_t)K * ns;
+            // snapshot P_jj = accumulator + the r pending terms [t, t + r)
+            uint32_t s0 = run.a0, s1 = run.a1;
+            const uint32_t rmax = __reduce_max_sync(0xffffffffu, r);
             #pragma unroll 1
-            for (uint32_t k = 0; k < nsingle; k++) {
-                const bool inA = k < r, inB = cont && k >= r;
+            for (uint32_t k = 0; k < rmax; k++) {
                 const uint32_t w = Run::term_w(mo, (uint32_t)(t + k));
-                const uint32_t s0 = inB ? b0 : run.a0, s1 = inB ? b1 : run.a1;
                 const uint32_t n1 = mo.mul2add<BIG>(s1, w, s0, mo.r1);
                 const uint32_t n0 = mo.mul(s0, w);
-                if (inB) { b0 = n0; b1 = n1; }
-                else if (inA) { run.a0 = n0; run.a1 = n1; }
+                const bool act = k < r;
+                s1 = act ? n1 : s1;
+                s0 = act ? n0 : s0;
             }
-            if (anycont) run.template advance<BIG>(mo, cont);
-            nterms += cnt + (cont ? K - r : 0u);       // this sum's portion + the next sum's first K - r terms
-            if (cont) { t += K; tp = t; }
-            else t += r;                               // leftover singles: the table stays at tp
             if (valid) {
-                const uint32_t c1 = mo.mul(run.a1, lane_coef(mo, c_terms[cg.off + jj], rho));   // fold a_j
-                const uint32_t m1 = mo.mul2add<true>(C0, c1, C1, run.a0);                   // eqnCombinePairs
-                C0 = mo.mul(C0, run.a0);
+                nterms += (uint64_t)K * ns + (jj == je ? r : 0u);     // pending terms count where absorbed
+                // Abel weight: a_jj - a_{jj+1} inside the chain, a_J for its last sum
+                const uint32_t wgt = jj < je ? mo.sub(coef, coef_n) : coef;
+                const uint32_t c1 = mo.mul(s1, wgt);
+                const uint32_t m1 = mo.mul2add<true>(C0, c1, C1, s0);            // eqnCombinePairs
+                C0 = mo.mul(C0, s0);
                 C1 = m1;
             }
-            run.a0 = cont ? b0 : mo.r1;
-            run.a1 = cont ? b1 : 0u;
+            coef = coef_n;
+            // next sum not contiguous for this lane (or the slice ended): absorb the pending terms
+            // and continue at the next sum's first term (its table is realigned above)
+            if (jj < je && valid && fc != t + r) {
+                run.a0 = s0;
+                run.a1 = s1;
+                nterms += r;
+                if (t + r >= hi) {                      // the slice ended: nothing left to step
+                    t = tp = hi;
+                } else {
+                    t = fc > t + r ? fc : t + r;
+                }
+            }
         }
         j = je + 1;
     }

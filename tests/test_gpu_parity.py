@@ -289,7 +289,7 @@ def test_lane2_slicing_bit_exact(wv, items, monkeypatch):
 
 @pytest.mark.parametrize("chain", ["0", "1", "4"])
 def test_lane2_chain_modes_bit_exact(wv, chain, monkeypatch):
-    """Chain mode (one difference table through adjacent sums, straddling K-term steps) is on by default
+    """Chain mode (one table and one accumulator through adjacent sums, summation by parts) is on by default
     (e = 2 and e = 3 four-term steps: WV_LANE_CHAIN = 5); no chains with W pair steps (0), e = 2 only (1)
     and e = 3 only (4) must give the same residues on windows where
     sums are a few terms long (BB30 / EE33 just above 4096: empty, one- and two-term sums) and on a
