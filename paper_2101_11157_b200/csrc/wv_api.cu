@@ -51,7 +51,7 @@ struct GenTerm { uint32_t neg; uint64_t hi, lo; uint32_t xn, xd, yn, yd; };
 struct GenTier { const char *name; int test; uint64_t th; };
 static GenTier kGenTiers[] = {
     {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 1ull << 29}, {"BG_BIG", 0, 1ull << 24},
-    {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 27}, {"EG_BIG", 1, 1ull << 24},
+    {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 21}, {"EG_BIG", 1, 1ull << 24},
 };
 
 // uniform host copy of every congruence: headers + one term array (uploaded per device)
