@@ -50,8 +50,8 @@ struct GenTerm { uint32_t neg; uint64_t hi, lo; uint32_t xn, xd, yn, yd; };
 // generated-congruence tiers (name, test, threshold): names from congruences_gen.inc
 struct GenTier { const char *name; int test; uint64_t th; };
 static GenTier kGenTiers[] = {
-    {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 1ull << 29}, {"BG_BIG", 0, 1ull << 24},
-    {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 21}, {"EG_BIG", 1, 1ull << 24},
+    {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 1ull << 29}, {"BG_XL", 0, 1ull << 24}, {"BG_BIG", 0, 1ull << 30},
+    {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 21}, {"EG_XL", 1, 1ull << 24}, {"EG_BIG", 1, 1ull << 30},
 };
 
 // uniform host copy of every congruence: headers + one term array (uploaded per device)

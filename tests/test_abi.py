@@ -65,7 +65,7 @@ def test_host_utilities(pkg):
     assert names[pkg.schedule(10 ** 6, pkg.MODE_W)] == "BG_SML" and names[pkg.schedule(10 ** 6, pkg.MODE_V)] == "EG_SML"
     # generated many-sum congruences (NEXT-2) for large p (BIG from 2^24)
     assert names[pkg.schedule(10 ** 7, pkg.MODE_W)] == "BG_SML" and names[pkg.schedule(10 ** 7, pkg.MODE_V)] == "EG_MID"
-    assert names[pkg.schedule(10 ** 9, pkg.MODE_W)] == "BG_BIG" and names[pkg.schedule(10 ** 9, pkg.MODE_V)] == "EG_BIG"
+    assert names[pkg.schedule(10 ** 9, pkg.MODE_W)] == "BG_XL" and names[pkg.schedule(10 ** 9, pkg.MODE_V)] == "EG_XL"
     assert names[pkg.schedule(5 * 10 ** 10, pkg.MODE_W)] == "BG_BIG"
     assert names[pkg.schedule(5 * 10 ** 10, pkg.MODE_V)] == "EG_BIG"
     with pytest.raises(pkg.WVError):
