@@ -456,21 +456,30 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             j = je + 1;
             continue;
         }
+        // a slice (Q > 1) starts inside the chain: its sums that end before every lane's slice start add
+        // nothing (empty running sum), so only their bounds are computed
+        uint32_t j0 = j;
+        while (j0 < je && !__any_sync(0xffffffffu, valid && fc + nc > lo)) {
+            j0++;
+            if (valid) lane_bounds(mo.p, c_terms[cg.off + j0], c_termr[cg.off + j0], fc, nc);
+        }
         Run run;
         run.setup(mo, (uint32_t)lo);
         uint64_t t = lo, tp = lo;                     // accumulator covers [lo, t); the table sits at tp
-        uint32_t coef = valid ? lane_coef(mo, c_terms[cg.off + j], rho) : 0u;
-        for (uint32_t jj = j; jj <= je; jj++) {
+        uint32_t coef = valid ? lane_coef(mo, c_terms[cg.off + j0], rho) : 0u;
+        bool done = false;                            // this lane's slice ended in an earlier sum
+        for (uint32_t jj = j0; jj <= je; jj++) {
+            const bool act = valid && !done;
             const uint64_t f = fc;
             const uint32_t n = nc;
             uint32_t coef_n = 0;
-            if (jj < je && valid) {
+            if (jj < je && act) {
                 lane_bounds(mo.p, c_terms[cg.off + jj + 1], c_termr[cg.off + jj + 1], fc, nc);
                 coef_n = lane_coef(mo, c_terms[cg.off + jj + 1], rho);
             }
-            if (__any_sync(0xffffffffu, valid && t != tp)) {          // realign every lane's table at t
+            if (__any_sync(0xffffffffu, act && t != tp)) {            // realign every lane's table at t
                 const uint32_t s0 = run.a0, s1 = run.a1;
-                run.setup(mo, (uint32_t)(valid ? t : 1));
+                run.setup(mo, (uint32_t)(act ? t : 1));
                 run.a0 = s0;
                 run.a1 = s1;
                 tp = t;
@@ -478,7 +487,7 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             // this sum's end within the slice; steps of K while they fit, r < K terms left over
             uint64_t b = f + n < hi ? f + n : hi;
             if (b < t) b = t;
-            const uint32_t cnt = valid ? (uint32_t)(b - t) : 0u;
+            const uint32_t cnt = act ? (uint32_t)(b - t) : 0u;
             const uint32_t ns = cnt / K, r = cnt - ns * K;
             const uint32_t kmin = __reduce_min_sync(0xffffffffu, valid ? ns : 0xffffffffu);
             const uint32_t kmax = __reduce_max_sync(0xffffffffu, valid ? ns : 0u);
@@ -508,19 +517,24 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
                 s1 = act ? n1 : s1;
                 s0 = act ? n0 : s0;
             }
-            if (valid) {
-                nterms += (uint64_t)K * ns + (jj == je ? r : 0u);     // pending terms count where absorbed
-                // Abel weight: a_jj - a_{jj+1} inside the chain, a_J for its last sum
-                const uint32_t wgt = jj < je ? mo.sub(coef, coef_n) : coef;
+            // the slice ends in this sum (or the chain does): every later running sum equals this one,
+            // so their Abel weights telescope to a_jj and the lane is done with the chain
+            const bool last = jj == je || f + n >= hi;
+            if (act) {
+                nterms += (uint64_t)K * ns + (last ? r : 0u);         // pending terms count where absorbed
+                // Abel weight: a_jj - a_{jj+1} inside the chain, a_jj where the slice or chain ends
+                const uint32_t wgt = last ? coef : mo.sub(coef, coef_n);
                 const uint32_t c1 = mo.mul(s1, wgt);
                 const uint32_t m1 = mo.mul2add<true>(C0, c1, C1, s0);            // eqnCombinePairs
                 C0 = mo.mul(C0, s0);
                 C1 = m1;
+                done = last;
             }
+            if (__all_sync(0xffffffffu, !valid || done)) break;
             coef = coef_n;
-            // next sum not contiguous for this lane (or the slice ended): absorb the pending terms
-            // and continue at the next sum's first term (its table is realigned above)
-            if (jj < je && valid && fc != t + r) {
+            // next sum not contiguous for this lane: absorb the pending terms and continue at the next
+            // sum's first term (its table is realigned above)
+            if (jj < je && act && fc != t + r) {
                 run.a0 = s0;
                 run.a1 = s1;
                 nterms += r;
