@@ -416,12 +416,12 @@ __constant__ uint32_t c_lane_chain = 5u;   // bit 0: chain mode for e = 2; bit 2
 // enter the accumulator with the next step.  Per sum: bounds, coefficient, < K singles, one fold +
 // merge -- no table set-up and no accumulator restart.  (The generated congruences have 91 / 87 sums
 // in 47 / 24 chains (BG_SML / EG_SML), 3534 / 3535 in 1192 / 1065 (BG_BIG / EG_BIG).)
-// Every lane of the warp must have the same congruence (the caller checks).  Slices cut each chain's
-// integer range [F, E) into Q pieces (prefix sums over the slice's terms; the identity holds for any
-// P sequence).  A lane whose next sum does not start where its previous one ended (p < 7, R5) absorbs
+// Every lane of the warp must have the same congruence (the caller checks).  Slices cut the lane's
+// terms of all chains, concatenated in chain order, into Q pieces (prefix sums over the slice's terms;
+// the identity holds for any P sequence).  A lane whose next sum does not start where its previous one ended (p < 7, R5) absorbs
 // its pending terms and realigns its table there; a realignment sets up every lane's table at its
 // own position (accumulators kept).
-template <class Run, bool BIG>
+template <class Run, bool BIG, bool SL>     // SL: the item is a slice (Q > 1); Q == 1 compiles without the cut
 __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg, bool valid, uint64_t q, uint64_t Q,
                                                  double rQ, uint32_t &C0, uint32_t &C1, uint64_t &nterms) {
     constexpr uint32_t K = Run::K;
@@ -431,8 +431,29 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
     rho[1] = mo.mul(mo.r2, mo.r2);
     rho[2] = mo.mul(rho[1], mo.r2);
     rho[3] = mo.mul(rho[2], mo.r2);
+    // slice q of Q: the lane's terms of all chains, concatenated in chain order, cut into Q pieces
+    // [g_lo, g_hi), so a slice sets up tables only for the chains it overlaps
+    uint64_t g_lo = 0, g_hi = 0, base = 0;
+    if (SL) {
+        uint64_t tot = 0;
+        if (valid) {
+            for (uint32_t a = 0; a < m;) {
+                uint32_t b = a;
+                while (b + 1 < m && (c_terms[cg.off + b].pad & 1u)) b++;
+                uint64_t f0, f1;
+                uint32_t n0, n1;
+                lane_bounds(mo.p, c_terms[cg.off + a], c_termr[cg.off + a], f0, n0);
+                lane_bounds(mo.p, c_terms[cg.off + b], c_termr[cg.off + b], f1, n1);
+                tot += f1 + n1 > f0 ? f1 + n1 - f0 : 0;
+                a = b + 1;
+            }
+        }
+        g_lo = fdiv(tot * q, (uint32_t)Q, rQ);
+        g_hi = fdiv(tot * (q + 1), (uint32_t)Q, rQ);
+    }
     uint32_t j = 0;
     while (j < m) {
+        if (SL && __all_sync(0xffffffffu, !valid || base >= g_hi)) break;   // past every lane's slice
         uint32_t je = j;
         while (je + 1 < m && (c_terms[cg.off + je].pad & 1u)) je++;
         uint64_t F = 1, E = 1;
@@ -447,10 +468,12 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             E = f1 + n1 > F ? f1 + n1 : F;
         }
         uint64_t lo = F, hi = E;
-        if (Q > 1) {
-            const uint64_t N = E - F;
-            lo = F + fdiv(N * q, (uint32_t)Q, rQ);
-            hi = F + fdiv(N * (q + 1), (uint32_t)Q, rQ);
+        if (SL) {
+            const uint64_t w = E - F;
+            const uint64_t a = g_lo > base ? g_lo - base : 0, b = g_hi > base ? g_hi - base : 0;
+            lo = F + (a < w ? a : w);
+            hi = F + (b < w ? b : w);
+            base += valid ? w : 0;
         }
         if (!__any_sync(0xffffffffu, valid && lo < hi)) {
             j = je + 1;
@@ -459,7 +482,7 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
         // a slice (Q > 1) starts inside the chain: its sums that end before every lane's slice start add
         // nothing (empty running sum), so only their bounds are computed
         uint32_t j0 = j;
-        while (j0 < je && !__any_sync(0xffffffffu, valid && fc + nc > lo)) {
+        while (SL && j0 < je && !__any_sync(0xffffffffu, valid && fc + nc > lo)) {
             j0++;
             if (valid) lane_bounds(mo.p, c_terms[cg.off + j0], c_termr[cg.off + j0], fc, nc);
         }
@@ -607,11 +630,21 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
             // (six-term steps, LaneRunP<3, 6> / <2, 6>, measured slower: C2 residue 17.3 / 15.7 ms vs 13.1)
             // (chains with W pair steps measured slower than without: C2 residue 13.64 vs 13.29 ms; no longer built)
             if (e == 3) {                                  // four-term W steps
-                if (big) lane2_chain_item<RunW, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
-                else lane2_chain_item<RunW, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                if (Q > 1) {
+                    if (big) lane2_chain_item<RunW, true, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                    else lane2_chain_item<RunW, false, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                } else {
+                    if (big) lane2_chain_item<RunW, true, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                    else lane2_chain_item<RunW, false, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                }
             } else {
-                if (big) lane2_chain_item<RunV, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
-                else lane2_chain_item<RunV, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                if (Q > 1) {
+                    if (big) lane2_chain_item<RunV, true, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                    else lane2_chain_item<RunV, false, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                } else {
+                    if (big) lane2_chain_item<RunV, true, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                    else lane2_chain_item<RunV, false, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
+                }
             }
         } else if (e == 3) {
             if (big) lane2_item<LaneRun3, true>(mo, cg, valid, q, Q, rQ, C0, C1, nterms);

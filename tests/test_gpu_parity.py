@@ -206,6 +206,28 @@ def test_shards_union_equals_whole(wv):
         assert tot == chk
 
 
+@pytest.mark.parametrize("nsh", [8])
+def test_c2_shards_bit_exact(wv, nsh):
+    """The bench's N-GPU split of C2 (interleaved blocks, default block size): each shard is a small
+    window, so the lane kernel cuts its groups into several slices (Q > 1); the merged residues equal
+    the oracle's on every prime and the shard checksums add up to the whole window's."""
+    w = CONFIGS["c2"]
+    gp, gw, gv, _ = _golden("c2")
+    parts, tot = [], 0
+    for s in range(nsh):
+        ds = wv.DeviceSearch(w.lo, w.hi, w.mode, s, nsh).run()
+        rw, rv = ds.res_np()
+        parts.append((ds.primes_np(), rw, rv))
+        tot = (tot + ds.checksum_int()) % (1 << 64)
+    p = np.concatenate([a for a, _, _ in parts])
+    order = np.argsort(p, kind="stable")
+    assert p[order].tolist() == gp.tolist()
+    _assert_equal(gp, np.concatenate([b for _, b, _ in parts])[order], gw, "W")
+    _assert_equal(gp, np.concatenate([c for _, _, c in parts])[order], gv, "V")
+    want_chk = sum(wv.checksum_term(int(a), int(b), int(c)) for a, b, c in zip(gp, gw, gv)) % (1 << 64)
+    assert tot == want_chk
+
+
 def test_edge_windows(wv):
     h, r = wv.search(100, 101, 3)
     assert len(r) == 0 and len(h) == 0
@@ -261,7 +283,7 @@ def test_kernel_variants_bit_identical(wv):
             wv.set_kernel_variant(c, -1)
 
 
-@pytest.mark.parametrize("items", ["0.001", "1000000"])
+@pytest.mark.parametrize("items", ["0.001", "3", "1000000"])
 def test_lane2_slicing_bit_exact(wv, items, monkeypatch):
     """Class-0 lane mode v2 cuts each group's sums into Q slices (one slice size per launch, from
     WV_LANE_ITEMS items per resident warp): whole sums (Q = 1) and the finest cut (Q up to 128) give the
