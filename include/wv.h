@@ -81,8 +81,11 @@ int wv_search(uint64_t lo, uint64_t hi, uint32_t mode,
  * every shard >= 32 blocks, at least 2^15;
  * any block must be a multiple of 2^15, the sieve segment); block b = [lo + b*block, ...)
  * is dealt to shards in rounds of nshards, alternating direction ("snake"
- * interleave: round j gives block j*N + s for even j and j*N + N-1-s for odd j
- * to shard s), which balances the growth of per-prime work with p.  *checksum
+ * interleave: round j gives block j*N + s - pad for even j and j*N + N-1-s - pad
+ * for odd j to shard s, where pad = (-nblocks) mod N virtual empty blocks sit
+ * below block 0 so that the rounds align with the top of the window and the one
+ * partial round holds the lightest blocks), which balances the growth of
+ * per-prime work with p.  *checksum
  * receives this shard's order-independent 64-bit checksum (wv_checksum_term
  * summed mod 2^64), so shard checksums add up to the unsharded one.
  * checksum may be NULL. */

@@ -301,7 +301,7 @@ static int ctx_get(DevCtx **out) {
         CK(cudaMalloc(&d_off, (nseg1 + 1) * 8));
         CK(cudaMalloc(&d_tiles, 64));
         CK(cudaMemcpy(d_boot, h_boot, sizeof h_boot, cudaMemcpyHostToDevice));
-        SegMap m{0, BASE0_HI, BASE0_HI, 0, 1, BASE0_HI / SIEVE_SPAN, 3};
+        SegMap m{0, BASE0_HI, BASE0_HI, 0, 1, BASE0_HI / SIEVE_SPAN, 3, 0};
         cudaStream_t st = c.stream;
         LAUNCH(sieve_segments_kernel, (unsigned)nseg1, SIEVE_THREADS, st, m, d_boot, nboot, nullptr, d_bitmap, d_cnt);
         LAUNCH(scan_tile_totals<uint64_t>, 1, SCAN_THREADS, st, d_cnt, nseg1, d_tiles);
@@ -430,16 +430,19 @@ static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, 
     L.lo = lo; L.hi = hi; L.block = block; L.mode = mode; L.shard = shard; L.nshards = nshards;
     L.ntests = mode == 3 ? 2 : 1;
     const uint64_t nblocks = (width + block - 1) / block;
-    // blocks j of this shard: shard_block(j, shard, nshards) < nblocks (rounds of nshards, snake order)
-    uint64_t my_blocks = nblocks / nshards;
-    if (shard_block(my_blocks, shard, nshards) < nblocks) my_blocks++;
+    // blocks j of this shard: shard_block(j, shard, nshards) - pad (rounds of nshards, snake order,
+    // aligned to the top of the window; virtual blocks below 0 are empty)
+    const uint64_t pad = shard_pad(nblocks, nshards);
+    const uint64_t my_blocks = (nblocks + pad) / nshards;
     const uint64_t spb = block / SIEVE_SPAN;
-    L.map = SegMap{lo, hi, block, shard, nshards, spb, 5};
+    L.map = SegMap{lo, hi, block, shard, nshards, spb, 5, pad};
     L.nseg = my_blocks * spb;
     // primes in this shard: sum of per-block bounds
     uint64_t cap = 0;
     for (uint64_t j = 0; j < my_blocks; j++) {
-        uint64_t bs = lo + shard_block(j, shard, nshards) * block;
+        const uint64_t vb = shard_block(j, shard, nshards);
+        if (vb < pad) continue;
+        uint64_t bs = lo + (vb - pad) * block;
         uint64_t be = bs + block < hi ? bs + block : hi;
         cap += prime_bound(be - bs);
     }
@@ -454,7 +457,7 @@ static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, 
     if (L.need_l1) {
         const uint64_t hi1 = r + 1;
         const uint64_t blk1 = (hi1 + SIEVE_SPAN - 1) / SIEVE_SPAN * SIEVE_SPAN;
-        L.map1 = SegMap{0, hi1, blk1, 0, 1, blk1 / SIEVE_SPAN, 3};
+        L.map1 = SegMap{0, hi1, blk1, 0, 1, blk1 / SIEVE_SPAN, 3, 0};
         L.nseg1 = blk1 / SIEVE_SPAN;
         L.nbase1_cap = prime_bound(hi1);
     }
@@ -1023,10 +1026,12 @@ extern "C" int wv_shard_blocks(uint64_t lo, uint64_t hi, uint32_t shard, uint32_
     Layout L;
     TRY(make_layout(lo, hi, 1, shard, nshards, block, L));
     const uint64_t nblocks = (hi - lo + L.block - 1) / L.block;
+    const uint64_t pad = shard_pad(nblocks, nshards);
     size_t k = 0;
-    for (uint64_t j = 0;; j++) {
-        const uint64_t b = shard_block(j, shard, nshards);
-        if (b >= nblocks) break;
+    for (uint64_t j = 0; j < (nblocks + pad) / nshards; j++) {
+        const uint64_t vb = shard_block(j, shard, nshards);
+        if (vb < pad) continue;
+        const uint64_t b = vb - pad;
         const uint64_t a_ = lo + b * L.block, z = a_ + L.block < hi ? a_ + L.block : hi;
         if (z <= a_) continue;
         if (out && k < cap) { out[2 * k] = a_; out[2 * k + 1] = z; }

@@ -31,9 +31,14 @@ constexpr uint32_t SIEVE_MED = 2048;              // phase-2 / phase-3 split
 // Block b of the window belongs to shard snake(b): blocks are dealt out in rounds of
 // nshards, alternating direction (0,1,..,N-1, N-1,..,1,0, ...), so that the linear
 // growth of per-prime work with p is balanced across shards.  The j-th block of
-// shard s is  j*N + (j even ? s : N-1-s).
+// shard s is  j*N + (j even ? s : N-1-s)  - pad.  The rounds are aligned to the top of the window:
+// pad = (-nblocks) mod N virtual (empty) blocks sit below block 0, so the one partial round holds
+// the lightest blocks (smallest p) rather than the heaviest.
 __host__ __device__ __forceinline__ uint64_t shard_block(uint64_t j, uint32_t s, uint32_t n) {
     return j * n + ((j & 1) ? (uint64_t)(n - 1 - s) : (uint64_t)s);
+}
+__host__ __device__ __forceinline__ uint64_t shard_pad(uint64_t nblocks, uint32_t n) {
+    return (n - nblocks % n) % n;
 }
 
 struct SegMap {             // segment index -> integer range, for a shard of blocks
@@ -42,10 +47,16 @@ struct SegMap {             // segment index -> integer range, for a shard of bl
     uint32_t shard, nshards;
     uint64_t segs_per_block;
     uint64_t minp;          // smallest prime to report (5 for the search, 3 for base lists)
+    uint64_t pad;           // virtual empty blocks below block 0 (shard_pad)
 
     __host__ __device__ void range(uint64_t seg, uint64_t *a, uint64_t *b) const {
         uint64_t j = seg / segs_per_block, r = seg % segs_per_block;
         uint64_t blk = shard_block(j, shard, nshards);
+        if (blk < pad) {                          // virtual block: empty
+            *a = *b = lo;
+            return;
+        }
+        blk -= pad;
         uint64_t bs = lo + blk * block;           // may exceed hi for trailing segments
         uint64_t s = bs + r * (uint64_t)SIEVE_SPAN;
         uint64_t e = s + SIEVE_SPAN;

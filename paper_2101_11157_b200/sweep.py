@@ -43,13 +43,13 @@ def gpu_block_evaluator(lo: int, hi: int, mode: int, near_bound: int):
 def blocks_of(lo: int, hi: int, block: int, shard: int = 0, nshards: int = 1):
     """This shard's blocks in sweep order (snake interleave; see include/wv.h wv_search_shard)."""
     nb = (hi - lo + block - 1) // block
-    out, j = [], 0
-    while True:
-        b = j * nshards + ((nshards - 1 - shard) if (j & 1) else shard)
-        if b >= nb:
-            return out
-        out.append((lo + b * block, min(lo + (b + 1) * block, hi)))
-        j += 1
+    pad = (-nb) % nshards          # rounds aligned to the top of the window (virtual empty blocks below 0)
+    out = []
+    for j in range((nb + pad) // nshards):
+        b = j * nshards + ((nshards - 1 - shard) if (j & 1) else shard) - pad
+        if b >= 0:
+            out.append((lo + b * block, min(lo + (b + 1) * block, hi)))
+    return out
 
 
 def new_state(lo, hi, mode, block, near_bound, shard=0, nshards=1) -> dict:
