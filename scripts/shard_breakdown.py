@@ -9,7 +9,7 @@ from paper_2101_11157_b200.workloads import CONFIGS
 w = CONFIGS["c2"]
 blocks = [int(b) for b in os.environ.get("BLOCKS", "0").split(",")]
 for blk in blocks:
-    for n in (1, 8):
+    for n in [int(x) for x in os.environ.get("NS", "1,8").split(",")]:
         rows = []
         for shard in range(n):
             ds = wv.DeviceSearch(w.lo, w.hi, w.mode, shard, n, block=blk) if blk else wv.DeviceSearch(w.lo, w.hi, w.mode, shard, n)
