@@ -572,6 +572,9 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
                    (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr, segidx, L.segstride, LANE_SLICE,
                    LANE_QMAX, (lane && lane2) ? (unsigned long long *)(misc + M_LANE_T) : nullptr);
             if (lane && lane2 && L.ngt > 0) {
+                const uint64_t nbw = (L.ngt * 32 + 255) / 256;
+                LAUNCH(lane_group_terms_kernel, (unsigned)(nbw < (uint64_t)c->sms * 16 ? nbw : c->sms * 16), 256, st,
+                       primes, n_dev, n_host, mode, g_sched, L.ngt, gq, (unsigned long long *)(misc + M_LANE_T));
                 const uint64_t nb = (L.ngt + 255) / 256;
                 LAUNCH(lane_slices_kernel, (unsigned)(nb < (uint64_t)c->sms * 8 ? nb : c->sms * 8), 256, st, gq, L.ngt,
                        L.ntests, recs, K, nch, (const unsigned long long *)(misc + M_LANE_T), lane_items, 4096ull,

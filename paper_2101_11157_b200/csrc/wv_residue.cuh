@@ -206,8 +206,8 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
             const uint64_t pl = primes[il];
             const int cl = schedule(sched, pl, (int)test);
             uint64_t Tl = 0;
-            if (lane_total && i != 32 * g) {
-                // lane mode v2: only the group's first record publishes the group's term count
+            if (lane_total) {
+                // lane mode v2: the group's term count comes from lane_group_terms_kernel (one warp per group)
             } else if (il == i && cl == cid && !lane2rec) {
                 Tl = T;                                          // this record is the group's last prime
             } else if (cl >= 0 && cl < c_ncong) {
@@ -218,12 +218,9 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
                 }
             }
             if (lane_total) {
-                // deferred: gq = the group's term count, converted to slices by lane_slices_kernel
+                // deferred: gq = the group's term count (lane_group_terms_kernel), converted to slices by
+                // lane_slices_kernel
                 nc = 1;
-                if (i == 32 * g) {
-                    gq[g * ntests + (mode == 3 ? test : 0)] = Tl;
-                    atomicAdd(lane_total, (unsigned long long)Tl);
-                }
             } else {
                 uint64_t Q = (Tl + lane_slice - 1) / lane_slice;
                 if (Q < 1) Q = 1;
@@ -247,6 +244,40 @@ __global__ void plan_kernel(const uint64_t *__restrict__ primes, const uint64_t 
              gt += (uint64_t)gridDim.x * blockDim.x) {
             const uint64_t i0 = (gt / ntests) * 32;
             if (i0 >= n || primes[i0] >= WIDTH32_MAX) gq[gt] = 0;
+        }
+    }
+}
+
+// Lane mode v2, after plan_kernel: the term count of each class-0 group-test (the group's last prime, whose
+// congruence and counts bound the group's), one warp per group-test with the lanes striding over the
+// sums -> gq[gt], and their total -> lane_total.  Groups plan_kernel marked non-class-0 (gq = 0) are skipped.
+__global__ void lane_group_terms_kernel(const uint64_t *__restrict__ primes, const uint64_t *__restrict__ n_primes_dev,
+                                        uint64_t n_primes_host, uint32_t mode, Sched sched, uint64_t ngt,
+                                        uint64_t *__restrict__ gq, unsigned long long *__restrict__ lane_total) {
+    const uint32_t ntests = (mode == 3) ? 2 : 1;
+    const uint64_t n = n_primes_dev ? *n_primes_dev : n_primes_host;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t gt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gt < ngt; gt += nw) {
+        const uint64_t i0 = 32 * (gt / ntests);
+        if (i0 >= n || primes[i0] >= WIDTH32_MAX) continue;          // warp-uniform
+        const uint32_t test = (mode == 3) ? (uint32_t)(gt % ntests) : (mode == 1 ? 0u : 1u);
+        const uint64_t pl = primes[i0 + 31 < n ? i0 + 31 : n - 1];
+        const int cl = schedule(sched, pl, (int)test);
+        uint64_t Tl = 0;
+        if (cl >= 0 && cl < c_ncong) {
+            const Cong &c = c_cong[cl];
+            for (uint32_t jj = lane; jj < c.m; jj += 32) {
+                uint64_t f, cnt;
+                sum_bounds_r(pl, c_terms[c.off + jj], c_termr[c.off + jj], &f, &cnt);
+                Tl += cnt;
+            }
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) Tl += __shfl_xor_sync(0xffffffffu, Tl, o);
+        if (lane == 0) {
+            gq[gt] = Tl;
+            atomicAdd(lane_total, (unsigned long long)Tl);
         }
     }
 }
