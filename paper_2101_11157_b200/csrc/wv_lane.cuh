@@ -542,7 +542,7 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             }
             // the slice ends in this sum (or the chain does): every later running sum equals this one,
             // so their Abel weights telescope to a_jj and the lane is done with the chain
-            const bool last = jj == je || f + n >= hi;
+            const bool last = jj == je || (SL && f + n >= hi);
             if (act) {
                 nterms += (uint64_t)K * ns + (last ? r : 0u);         // pending terms count where absorbed
                 // Abel weight: a_jj - a_{jj+1} inside the chain, a_jj where the slice or chain ends
@@ -553,7 +553,7 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
                 C1 = m1;
                 done = last;
             }
-            if (__all_sync(0xffffffffu, !valid || done)) break;
+            if (SL && __all_sync(0xffffffffu, !valid || done)) break;
             coef = coef_n;
             // next sum not contiguous for this lane: absorb the pending terms and continue at the next
             // sum's first term (its table is realigned above)
