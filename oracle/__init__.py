@@ -12,10 +12,12 @@ Tiers (see wv_oracle.c for the cited passages):
   O(p^2), used for p <= 2000 (and in pins up to a few 10^4); it yields every
   index 2k <= p-3 at once, so it is also the oracle of the general-index census
   (``index_residues``, SURVEY.md 8(f) NEXT-3);
-* tier B  -- W: sum_{k<p} k^-2 mod p^2 (eqnWolst + Glaisher), p < 2^32;
+* tier B  -- W: sum_{k<p} k^-2 mod p^2 (eqnWolst + Glaisher): one 64-bit word
+  for p < 2^32, base-p digit pairs for 2^32 <= p < 2^62;
   V: Glaisher's quarter sum, -4 E_{p-3} == sum_{s<p/4} s^-2 (DESIGN.md R1);
-* tier C  -- W for p >= 2^32: Stafford-Vandiver eqnSV == eqnBB1
-  (21 B_{p-3} == sum_{p/6<s<p/4} s^-3).
+* tier C  -- cross-check pin only: Stafford-Vandiver eqnSV == eqnBB1
+  (21 B_{p-3} == sum_{p/6<s<p/4} s^-3), the paper's own reduced congruence;
+  never the oracle of a prime.
 
 All functions return canonical residues in [0, p).
 """
@@ -23,6 +25,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import multiprocessing
 import subprocess
 from concurrent.futures import ProcessPoolExecutor
 
@@ -32,6 +35,9 @@ _LIB = os.path.join(_HERE, "_liboracle.so")
 _BAD = (1 << 64) - 1
 
 _lib = None
+# Worker processes are spawned, never forked: the callers (pytest -m gpu, smoke, bench) hold an
+# initialised CUDA context, which a forked child must not inherit.
+_SPAWN = multiprocessing.get_context("spawn")
 
 
 def build(force: bool = False) -> str:
@@ -52,7 +58,7 @@ def _load():
         p64 = ctypes.POINTER(ctypes.c_uint64)
         for name in ("oracle_residue_B", "oracle_residue_E", "oracle_B_harmonic", "oracle_B_glaisher",
                      "oracle_E_quarter", "oracle_quarter_sum", "oracle_B_stafford_vandiver",
-                     "oracle_wolstenholme_h2"):
+                     "oracle_wolstenholme_h2", "oracle_B_harmonic_wide"):
             f = getattr(lib, name)
             f.argtypes = [u64]
             f.restype = u64
@@ -64,6 +70,10 @@ def _load():
         lib.oracle_primes.restype = u64
         lib.oracle_binom_2p_1_mod_p4.argtypes = [u64, p64, p64]
         lib.oracle_binom_2p_1_mod_p4.restype = ctypes.c_int
+        lib.oracle_wolstenholme_h2_wide.argtypes = [u64, p64, p64]
+        lib.oracle_wolstenholme_h2_wide.restype = ctypes.c_int
+        lib.oracle_p2_mul.argtypes = [u64, u64, u64, u64, u64, p64, p64]
+        lib.oracle_p2_mul.restype = ctypes.c_int
         lib.oracle_invmod.argtypes = [u64, u64]
         lib.oracle_invmod.restype = u64
         lib.oracle_mulmod.argtypes = [u64, u64, u64]
@@ -126,6 +136,26 @@ def B_harmonic(p: int) -> int:
     return _chk(_load().oracle_B_harmonic(p))
 
 
+def wolstenholme_h2_wide(p: int) -> int:
+    """sum_{0<k<p} k^-2 mod p^2 in base-p digit arithmetic (5 <= p < 2^62)."""
+    d0, d1 = ctypes.c_uint64(), ctypes.c_uint64()
+    if _load().oracle_wolstenholme_h2_wide(p, ctypes.byref(d0), ctypes.byref(d1)) != 0:
+        raise ValueError("oracle: p outside [5, 2^62)")
+    return d0.value + d1.value * p
+
+
+def B_harmonic_wide(p: int) -> int:
+    return _chk(_load().oracle_B_harmonic_wide(p))
+
+
+def p2_mul(a: int, b: int, p: int) -> int:
+    """a*b mod p^2 through the oracle's base-p long multiplication (a, b < p^2)."""
+    r0, r1 = ctypes.c_uint64(), ctypes.c_uint64()
+    if _load().oracle_p2_mul(a % p, a // p, b % p, b // p, p, ctypes.byref(r0), ctypes.byref(r1)) != 0:
+        raise ValueError("oracle: operands outside the digit domain")
+    return r0.value + r1.value * p
+
+
 def B_glaisher(p: int) -> int:
     return _chk(_load().oracle_B_glaisher(p))
 
@@ -179,7 +209,7 @@ def residues(plist, mode: int = 3, workers: int | None = None):
     if workers == 1 or len(plist) < 2:
         return [_one((p, mode)) for p in plist]
     _load()
-    with ProcessPoolExecutor(max_workers=workers) as ex:
+    with ProcessPoolExecutor(max_workers=workers, mp_context=_SPAWN) as ex:
         return list(ex.map(_one, [(p, mode) for p in plist], chunksize=max(1, len(plist) // (workers * 16))))
 
 
@@ -204,7 +234,7 @@ def index_residues_many(plist, workers: int | None = None):
     if workers == 1 or len(plist) < 2:
         return dict(_index_one(p) for p in plist)
     _load()
-    with ProcessPoolExecutor(max_workers=workers) as ex:
+    with ProcessPoolExecutor(max_workers=workers, mp_context=_SPAWN) as ex:
         return dict(ex.map(_index_one, plist, chunksize=1))
 
 

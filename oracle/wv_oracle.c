@@ -22,21 +22,27 @@
  *     W: the first congruence of eqnWolst in its exact mod-p^2
  *        form  sum_{0<k<p} k^{-2} == (2/3) p B_{p-3}  (mod p^2)  (Glaisher;
  *        the "strengthening" equivalence stated at P:L45-50 with the
- *        residue made explicit by eqnGlaisher); p < 2^32.
+ *        residue made explicit by eqnGlaisher).  For p < 2^32 the
+ *        residues mod p^2 fit one 64-bit word; for 2^32 <= p < 2^62 they are
+ *        held as two base-p digits (schoolbook long multiplication, below).
+ *        This is the W oracle for every p > 2000.
  *     W (pin only): eqnGlaisher itself with h = 2,
  *        C(2p-1, p-1) == 1 - (2/3) p^3 B_{p-3}  (mod p^4); p < 2^31.
  *     V: Glaisher's quarter-range formula eqnE1 at k = 1 (P:L748-756,
  *        section 4), with the sign reading of DESIGN.md "Readings" R1:
  *        -4 E_{p-3} == sum_{0<s<p/4} s^{-2}  (mod p).
- *   tier C (p >= 2^32, W only): the Stafford-Vandiver congruence eqnSV
- *         at k = (p-3)/2, i.e. eqnBB1:
- *        21 B_{p-3} == sum_{p/6<s<p/4} s^{-3}  (mod p).
+ *   tier C (cross-check pin only, never dispatched): the Stafford-Vandiver
+ *        congruence eqnSV at k = (p-3)/2, i.e. eqnBB1:
+ *        21 B_{p-3} == sum_{p/6<s<p/4} s^{-3}  (mod p).  It is one of the
+ *        paper's own reduced congruences, so it is kept only to be compared
+ *        with tier B (tests), not as the oracle of any prime.
  *
  * Sums of inverses are accumulated as one fraction num/den, adding 1/u by
  * num/den + 1/u = (num*u + den)/(den*u) (all mod the modulus), with a single
  * modular inverse at the end: the schoolbook rule for adding fractions.
  *
- * Arithmetic is exact: unsigned 64-bit residues, 128-bit products, '%'.
+ * Arithmetic is exact: unsigned 64-bit residues, 128-bit products, '%' and
+ * '/' (for p^2 >= 2^64: base-p digit pairs, products by long multiplication).
  * Functions return UINT64_MAX when an argument is outside their domain.
  */
 #include <stdint.h>
@@ -213,6 +219,87 @@ u64 oracle_B_harmonic(u64 p)
 }
 
 /* ------------------------------------------------------------------ */
+/* tier B, W for 2^32 <= p < 2^62: the same sum mod p^2 in base p       */
+/* ------------------------------------------------------------------ */
+/* A residue x mod p^2 is held as its two base-p digits, x = d0 + d1 p with
+ * 0 <= d0, d1 < p.  Long multiplication in base p, dropping the p^2 column:
+ *   (a0 + a1 p)(b0 + b1 p) = a0 b0 + (a0 b1 + a1 b0) p + a1 b1 p^2
+ *                          == c0 + ((c1 + a0 b1 + a1 b0) mod p) p   (mod p^2),
+ * where a0 b0 = c1 p + c0 (quotient and remainder).  For p < 2^62 every
+ * intermediate is below 2p^2 + p < 2^126: exact in unsigned 128-bit. */
+typedef struct { u64 d0, d1; } p2num;
+
+static p2num p2_from(u128 x, u64 p)            /* x < p^2 */
+{
+    p2num r = { (u64)(x % p), (u64)(x / p) };
+    return r;
+}
+
+static p2num p2_mul(p2num a, p2num b, u64 p)
+{
+    u128 t = (u128)a.d0 * b.d0;
+    u64 c1 = (u64)(t / p);
+    u64 c0 = (u64)(t - (u128)c1 * p);
+    u128 col1 = (u128)a.d0 * b.d1 + (u128)a.d1 * b.d0 + c1;
+    p2num r = { c0, (u64)(col1 % p) };
+    return r;
+}
+
+static p2num p2_add(p2num a, p2num b, u64 p)    /* digit-wise with carry */
+{
+    u64 d0 = a.d0 + b.d0, carry = 0;
+    if (d0 >= p) { d0 -= p; carry = 1; }
+    u64 d1 = a.d1 + b.d1 + carry;
+    if (d1 >= p) d1 -= p;
+    p2num r = { d0, d1 };
+    return r;
+}
+
+/* exported for the pins: (a0 + a1 p)(b0 + b1 p) mod p^2 as digits */
+int oracle_p2_mul(u64 a0, u64 a1, u64 b0, u64 b1, u64 p, u64 *r0, u64 *r1)
+{
+    if (p < 2 || p >= ((u64)1 << 62) || a0 >= p || a1 >= p || b0 >= p || b1 >= p) return -1;
+    p2num a = { a0, a1 }, b = { b0, b1 };
+    p2num r = p2_mul(a, b, p);
+    *r0 = r.d0; *r1 = r.d1;
+    return 0;
+}
+
+static u128 invmod128(u128 a, u128 m);
+
+/* H2 = sum_{0<k<p} k^{-2} mod p^2 for 5 <= p < 2^62, as digits (d0, d1).
+ * The same running fraction as oracle_wolstenholme_h2: k^2 < p^2 is reduced
+ * already; the single inverse of den (a unit mod p^2) is by Euclid on 128-bit
+ * integers. */
+int oracle_wolstenholme_h2_wide(u64 p, u64 *d0, u64 *d1)
+{
+    if (p < 5 || p >= ((u64)1 << 62)) return -1;
+    p2num num = { 0, 0 }, den = { 1, 0 };
+    for (u64 k = 1; k < p; k++) {
+        p2num u = p2_from((u128)k * k, p);
+        num = p2_add(p2_mul(num, u, p), den, p);
+        den = p2_mul(den, u, p);
+    }
+    u128 m = (u128)p * p;
+    u128 den_v = (u128)den.d1 * p + den.d0;
+    u128 inv = invmod128(den_v, m);
+    if (inv == 0) return -1;
+    p2num h = p2_mul(num, p2_from(inv, p), p);
+    *d0 = h.d0; *d1 = h.d1;
+    return 0;
+}
+
+/* B_{p-3} mod p from H2 == (2/3) p B_{p-3} (mod p^2): p | H2 (Wolstenholme,
+ * digit d0 = 0) and B_{p-3} == (3/2) d1 (mod p). */
+u64 oracle_B_harmonic_wide(u64 p)
+{
+    u64 d0, d1;
+    if (oracle_wolstenholme_h2_wide(p, &d0, &d1) != 0) return BAD;
+    if (d0 != 0) return BAD;           /* Wolstenholme's theorem fails: impossible */
+    return mulmod(mulmod(d1, 3, p), invmod(2, p), p);
+}
+
+/* ------------------------------------------------------------------ */
 /* tier B, W (pin): Glaisher's binomial congruence mod p^4            */
 /* ------------------------------------------------------------------ */
 /* a*b mod m for m < 2^127, by shift-and-add (schoolbook binary method). */
@@ -334,7 +421,7 @@ u64 oracle_residue_B(u64 p)
     if (p < 5) return BAD;
     if (p <= TIER_A_MAX) return oracle_bernoulli_mod_p(p, p - 3, NULL);
     if (p < ((u64)1 << 32)) return oracle_B_harmonic(p);
-    return oracle_B_stafford_vandiver(p);
+    return oracle_B_harmonic_wide(p);
 }
 
 u64 oracle_residue_E(u64 p)

@@ -1,8 +1,12 @@
 """Multi-GPU search: one process per GPU, interleaved prime blocks, NCCL gather of results.
 
-SURVEY.md 8(e): [lo, hi) is cut into fixed blocks; block b belongs to rank
-b mod N (interleaved for load balance: prime density and per-prime work both
-drift with p).  Each rank sieves and computes its own blocks with no
+SURVEY.md 8(e): [lo, hi) is cut into fixed blocks dealt to the N ranks in
+rounds of N, snake order (round j gives block jN + r to rank r for even j and
+block jN + N-1-r for odd j), with the rounds aligned to the top of the window
+(pad = (-nblocks) mod N virtual empty blocks below block 0, so the one partial
+round holds the lightest blocks) -- wv_shard_blocks / wv_search_shard in
+include/wv.h.  Interleaving balances prime density and per-prime work, which
+both drift with p.  Each rank sieves and computes its own blocks with no
 communication (wv_search_shard on its device).  The only exchange is after
 compute: an all_gather of (n_primes, n_hits, checksum) per rank, then of the
 hit lists padded to the largest count (and, only if asked, of the residues).

@@ -24,6 +24,10 @@ import json
 import os
 
 M64 = (1 << 64) - 1
+# Block order of a shard.  Part of the configuration (and so of the digest): a checkpoint written
+# under another partition must not resume into this one's block list.
+PARTITION = "snake-top-v2"
+FORMAT = 2
 
 
 def _digest(cfg: dict) -> str:
@@ -54,7 +58,7 @@ def blocks_of(lo: int, hi: int, block: int, shard: int = 0, nshards: int = 1):
 
 def new_state(lo, hi, mode, block, near_bound, shard=0, nshards=1) -> dict:
     cfg = dict(lo=str(lo), hi=str(hi), mode=mode, block=str(block), near_bound=near_bound, shard=shard,
-               nshards=nshards, hist_bins=2000)
+               nshards=nshards, hist_bins=2000, partition=PARTITION, format=FORMAT)
     return dict(config=cfg, digest=_digest(cfg), next_block=0, blocks=len(blocks_of(lo, hi, block, shard, nshards)),
                 primes=0, checksum="0", hits=[], near=[], hist_w=[0] * 2000, hist_v=[0] * 2000, done=False)
 
@@ -75,10 +79,14 @@ def sweep(lo: int, hi: int, mode: int, block: int, state_path: str, near_bound: 
     if os.path.exists(state_path):
         with open(state_path) as f:
             old = json.load(f)
-        if old.get("digest") != state["digest"]:
-            raise ValueError(f"{state_path}: checkpoint belongs to another sweep configuration")
+        if old.get("digest") != state["digest"] or _digest(old.get("config", {})) != state["digest"]:
+            raise ValueError(f"{state_path}: checkpoint belongs to another sweep configuration "
+                             "(or another partition / format version)")
         state = old
     todo = blocks_of(lo, hi, block, shard, nshards)
+    if state["blocks"] != len(todo) or not 0 <= state["next_block"] <= len(todo):
+        raise ValueError(f"{state_path}: checkpoint has {state['blocks']} blocks (next {state['next_block']}), "
+                         f"this partition has {len(todo)}")
     done_now = 0
     while state["next_block"] < len(todo) and (max_blocks is None or done_now < max_blocks):
         a, b = todo[state["next_block"]]
@@ -103,6 +111,10 @@ def merge_states(states: list[dict]) -> dict:
     cfgs = {json.dumps({k: v for k, v in s["config"].items() if k not in ("shard",)}, sort_keys=True) for s in states}
     if len(cfgs) != 1:
         raise ValueError("states belong to different sweeps")
+    nshards = states[0]["config"]["nshards"]
+    if sorted(s["config"]["shard"] for s in states) != list(range(nshards)):
+        raise ValueError(f"merge needs each shard 0..{nshards - 1} exactly once, got "
+                         f"{sorted(s['config']['shard'] for s in states)}")
     cfg = dict(states[0]["config"], shard=0, nshards=1)
     out = dict(config=cfg, digest=_digest(cfg), done=all(s["done"] for s in states),
                primes=sum(s["primes"] for s in states),

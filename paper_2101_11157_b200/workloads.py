@@ -44,6 +44,8 @@ SUBWINDOWS = {
     "c5_head": Window("c5_head", 39 * 10 ** 9, 39 * 10 ** 9 + 10 ** 4, MODE_BOTH, "first 1e4 integers of C5"),
     "c5_scale": Window("c5_scale", 39 * 10 ** 9, 39 * 10 ** 9 + 4 * 10 ** 6, MODE_BOTH,
                        "first 4e6 integers of C5 (SURVEY.md 8(d) scaling sub-window)"),
+    "c5_frontier": Window("c5_frontier", 39 * 10 ** 9, 39 * 10 ** 9 + (1 << 15), MODE_BOTH,
+                          "bench.py frontier leg, rank 0's window (rank r: +r*2^15)"),
     "c2_probe": Window("c2_probe", 1 << 44, (1 << 44) + 60, MODE_W, "primes just above 2^44 (64-bit Montgomery class)"),
     "c3_slice": Window("c3_slice", 10 ** 9, 10 ** 9 + 5 * 10 ** 5, MODE_V, "first 5e5 integers of C3"),
     "c3_slice_both": Window("c3_slice_both", 10 ** 9, 10 ** 9 + 5 * 10 ** 5, MODE_BOTH, "first 5e5 integers of C3, W+V"),

@@ -481,3 +481,20 @@ def test_bench_contract_line():
     assert line["value"] > 1e5 and line["config"]["primes"] == 216814
     assert 0 < line["roofline"]["frac"] <= 1.5 and line["gpu_launches"] > 0
     assert line["e2e"]["d2h_bytes_per_step"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_frontier_window_primes_and_samples(wv):
+    """bench.py's frontier leg (C5 sub-window [3.9e10, 3.9e10 + 2^15), the FP64 engine): its prime list
+    equals the oracle's sieve, and every C5 oracle golden sample inside it is reproduced bit-exactly
+    through the same DeviceSearch path the bench times."""
+    w = SUBWINDOWS["c5_frontier"]
+    ds = wv.DeviceSearch(w.lo, w.hi, w.mode).run()
+    got = ds.primes_np()
+    assert got.tolist() == oracle.primes(w.lo, w.hi)
+    rw, rv = ds.res_np()
+    gp, gw, gv, _ = _golden("c5")
+    inside = (gp >= w.lo) & (gp < w.hi)
+    assert inside.sum() >= 1
+    idx = np.searchsorted(got, gp[inside])
+    _assert_equal(gp[inside], rw[idx], gw[inside], "frontier W")
+    _assert_equal(gp[inside], rv[idx], gv[inside], "frontier V")

@@ -146,8 +146,51 @@ def test_printed_glaisher_E1_sign_reading():
             assert printed == (-q) % p and q != 0
 
 
+def test_p2_long_multiplication_exact():
+    """The wide tier's base-p digit product (a0 + a1 p)(b0 + b1 p) mod p^2 equals Python's exact integer
+    a*b mod p^2 for seeded random operands and moduli up to 2^62 (both digit columns, carries > 2^64)."""
+    rng = random.Random(1157)
+    for bits in (20, 33, 36, 45, 61):
+        for _ in range(40):
+            p = rng.randrange(1 << (bits - 1), 1 << bits) | 1
+            a, b = rng.randrange(p * p), rng.randrange(p * p)
+            assert oracle.p2_mul(a, b, p) == a * b % (p * p), (p, a, b)
+        p = (1 << bits) - 1
+        assert oracle.p2_mul(p * p - 1, p * p - 1, p) == 1          # (-1)^2
+
+
+def test_wide_harmonic_matches_narrow_and_definition():
+    """Tier B in base-p digits (the W oracle for p >= 2^32) == the one-word tier B and the Bernoulli
+    recurrence (tier A) wherever those apply; H2 itself (not only its p-quotient) is compared."""
+    for p in _primes(5, 700):
+        assert oracle.B_harmonic_wide(p) == oracle.B_recurrence(p), p
+    rng = random.Random(3)
+    for _ in range(6):
+        p = int(sympy.nextprime(rng.randrange(10 ** 5, 2 * 10 ** 6)))
+        assert oracle.wolstenholme_h2_wide(p) == oracle.wolstenholme_h2(p), p
+        assert oracle.B_harmonic_wide(p) == oracle.B_harmonic(p), p
+    for p in _known()["wolstenholme_below_6e10"]:
+        assert oracle.B_harmonic_wide(p) == 0, p                  # H2 == 0 mod p^3 (P:L130-135)
+
+
+def test_table2_rows_above_2_32_from_definition():
+    """Table 2: the rows with p > 2^32, computed by oracle tier B in base-p digits
+    (sum k^-2 mod p^2 -- the definition-level W oracle of every C4/C5 prime) by the committed script
+    scripts/gen_wide_goldens.py, equal the printed symmetric residues, sign included."""
+    path = os.path.join(GOLD, "oracle_table2_wide.json")
+    if not os.path.exists(path):
+        pytest.skip("oracle_table2_wide.json not generated yet (scripts/gen_wide_goldens.py)")
+    with open(path) as f:
+        got = {int(p): r for p, r in json.load(f)["res_w"].items()}
+    rows = {int(r["p"]): int(r["symres_B"]) for r in _table("paper_table2_bernoulli.csv")}
+    above = [p for p in rows if p > (1 << 32)]
+    assert len(above) == 14 and set(got) == set(above)
+    for p in above:
+        assert oracle.symres(got[p], p) == rows[p], p
+
+
 def test_tier_B_and_C_agree_random():
-    """Stafford-Vandiver (eqnSV, tier C) == harmonic (tier B) on seeded random primes."""
+    """Stafford-Vandiver (eqnSV, tier C; pin only) == harmonic (tier B) on seeded random primes."""
     rng = random.Random(2101_11157)
     for _ in range(12):
         p = int(sympy.nextprime(rng.randrange(10 ** 4, 3 * 10 ** 6)))

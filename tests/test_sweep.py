@@ -65,3 +65,53 @@ def test_gpu_sweep_matches_search(tmp_path, wv):
     assert a["checksum"] == str(chk) and a["primes"] == len(res) == 9590
     assert [[str(int(h["p"])), int(h["flags"])] for h in hits] == a["hits"]
     assert sum(a["hist_w"]) == sum(a["hist_v"]) == 9590
+
+
+def test_merge_rejects_duplicate_or_missing_shards(tmp_path):
+    lo, hi, block = 3 * 10 ** 6, 3 * 10 ** 6 + 5 * 32768, 32768
+    parts = [sw.sweep(lo, hi, 3, block, str(tmp_path / f"s{r}.json"), shard=r, nshards=3, evaluate=_fake_eval)
+             for r in range(3)]
+    with pytest.raises(ValueError):
+        sw.merge_states([parts[0], parts[0], parts[1]])
+    with pytest.raises(ValueError):
+        sw.merge_states(parts[:2])
+    sw.merge_states([parts[2], parts[0], parts[1]])      # any order of the complete set
+
+
+def test_checkpoint_records_partition_and_block_count(tmp_path):
+    """A checkpoint names its partition (and format); one written under another partition, or whose
+    block count disagrees with this partition's, is refused instead of resumed into the wrong blocks."""
+    lo, hi, block = 10 ** 6, 10 ** 6 + 6 * 32768, 32768
+    path = tmp_path / "c.json"
+    s = sw.sweep(lo, hi, 3, block, str(path), shard=1, nshards=2, max_blocks=1, evaluate=_fake_eval)
+    assert s["config"]["partition"] == sw.PARTITION and s["config"]["format"] == sw.FORMAT
+    old = json.loads(path.read_text())
+    old["config"]["partition"] = "interleave-v1"
+    path.write_text(json.dumps(old))
+    with pytest.raises(ValueError):
+        sw.sweep(lo, hi, 3, block, str(path), shard=1, nshards=2, evaluate=_fake_eval)
+    s = sw.new_state(lo, hi, 3, block, 50, 1, 2)
+    s["blocks"] += 1
+    s["next_block"] = 1
+    path.write_text(json.dumps(s))
+    with pytest.raises(ValueError):
+        sw.sweep(lo, hi, 3, block, str(path), shard=1, nshards=2, evaluate=_fake_eval)
+
+
+def test_blocks_of_equals_library_partition():
+    """sweep.blocks_of (Python) and wv_shard_blocks (the C ABI that wv_search_shard uses) describe the
+    same partition, for ragged windows, several block sizes and shard counts (host-only call)."""
+    import __graft_entry__ as g
+    g.build()
+    from paper_2101_11157_b200 import _wv
+    import random
+    rng = random.Random(4)
+    for _ in range(40):
+        lo = rng.randrange(5, 10 ** 9)
+        block = 1 << rng.randrange(17, 21)
+        hi = lo + rng.randrange(1, 70) * block + rng.randrange(0, block)
+        n = rng.randrange(1, 9)
+        for r in range(n):
+            lib_blocks, used = _wv.shard_blocks(lo, hi, r, n, block)
+            assert used == block
+            assert [tuple(map(int, b)) for b in lib_blocks] == sw.blocks_of(lo, hi, block, r, n), (lo, hi, block, r, n)
