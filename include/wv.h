@@ -212,12 +212,15 @@ int wv_congruence_term(int id, uint32_t j, wv_term128 *out);
  * schedule).  The caller must respect validity (min_p / excluded_p); an
  * invalid forced choice for some p gives WV_EINVAL from the search. */
 int wv_set_schedule_override(int w_id, int v_id);
-/* Default schedule: W: p = 5 BB1, p = 7 VOR12, 11 <= p < 4096 BB1, p >= 4096 BB30;
- *                   V: p < 4096 EE3, p >= 4096 EE33;
- * then the generated congruences "BG_SML" / "EG_SML" (greedy continuations of BB30 / EE33,
- * p >= 2^17), and for large p the many-sum "BG_MID" (W, p >= 2^29),
- * "BG_BIG" (W, p >= 2^34), "EG_MID" (V, p >= 2^27), "EG_BIG" (V, p >= 2^32) when the
- * library was built with them (congruences_gen.inc).  Returns the id used. */
+/* Default schedule (each p takes the tier with the largest threshold <= p):
+ *   W: p = 5 BB1, p = 7 VOR12, 11 <= p < 4096 BB1, 4096 <= p < 2^17 BB30,
+ *      2^17 <= p < 2^24 "BG_SML", 2^24 <= p < 2^30 "BG_XL", p >= 2^30 "BG_BIG";
+ *   V: p < 4096 EE3, 4096 <= p < 2^17 EE33, 2^17 <= p < 2^21 "EG_SML",
+ *      2^21 <= p < 2^24 "EG_MID", 2^24 <= p < 2^30 "EG_XL", p >= 2^30 "EG_BIG";
+ * the quoted names are the generated congruences of congruences_gen.inc (greedy continuations of
+ * BB30 / EE33, and of eqnVandiver / eqnEMac2 for the many-sum tiers).  "BG_MID" is built but in no
+ * default range; WV_TH_<name> (read once) sets any generated tier's threshold (0 disables it).
+ * Returns the id used. */
 int wv_schedule(uint64_t p, uint32_t test /* WV_MODE_W or WV_MODE_V */);
 
 /* Measurement hooks (process-wide, for bench.py / profiling).  When enabled,

@@ -131,8 +131,35 @@ def _ptr(t):
 
 # ------------------------------------------------------------------ host-buffer API
 def search(lo: int, hi: int, mode: int = MODE_BOTH, residues: bool = True):
-    """wv_search: returns (hits: np.ndarray[HIT_DTYPE], residues: np.ndarray[RES_DTYPE] or None)."""
-    return search_shard(lo, hi, mode, 0, 1, 0, residues)[:2]
+    """wv_search: returns (hits: np.ndarray[HIT_DTYPE], residues: np.ndarray[RES_DTYPE] or None).
+
+    Buffers are sized from the library's prime bound (wv_device_workspace_bytes); on WV_ENOSPC (the
+    two-call contract of include/wv.h) they are resized to the reported counts and the call repeated."""
+    L = lib()
+    ws, cap = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(L.wv_device_workspace_bytes(lo, hi, mode, 0, 1, 0, ctypes.byref(ws), ctypes.byref(cap)))
+    nh_cap = npr_cap = max(int(cap.value), 1)
+    for _ in range(2):
+        hits = np.zeros(nh_cap, dtype=HIT_DTYPE)
+        res = np.zeros(npr_cap, dtype=RES_DTYPE) if residues else None
+        nh, npr = ctypes.c_size_t(), ctypes.c_size_t()
+        rc = L.wv_search(lo, hi, mode, _ptr(hits), len(hits), ctypes.byref(nh), _ptr(res),
+                         len(res) if residues else 0, ctypes.byref(npr))
+        if rc == WV_ENOSPC:
+            nh_cap, npr_cap = max(int(nh.value), 1), max(int(npr.value), 1)
+            continue
+        _check(rc)
+        return hits[: nh.value].copy(), (res[: npr.value].copy() if residues else None)
+    _check(rc)
+
+
+def search_raw(lo: int, hi: int, mode: int, hits: np.ndarray | None, res: np.ndarray | None):
+    """One wv_search call into the given buffers (tests of the WV_ENOSPC contract):
+    returns (rc, n_hits, n_primes) without raising."""
+    nh, npr = ctypes.c_size_t(), ctypes.c_size_t()
+    rc = lib().wv_search(lo, hi, mode, _ptr(hits), 0 if hits is None else len(hits), ctypes.byref(nh), _ptr(res),
+                         0 if res is None else len(res), ctypes.byref(npr))
+    return int(rc), int(nh.value), int(npr.value)
 
 
 def search_shard(lo: int, hi: int, mode: int, shard: int, nshards: int, block: int = 0, residues: bool = True,

@@ -30,8 +30,7 @@ using namespace wv;
 // ------------------------------------------------------------------ constants
 // default schedule: the printed congruences, plus generated many-sum ones (if present) for large p;
 // finalised in sched_init() once the generated table is known
-static Sched g_sched = {{{0, 4096, 0, 0, 0, 0}, {0, 4096, 0, 0, 0, 0}},
-                        {{C_BB1, C_BB30, 0, 0, 0, 0}, {C_EE3, C_EE33, 0, 0, 0, 0}}, {2, 2}, -1, -1};
+static Sched g_sched = {{{0, 4096}, {0, 4096}}, {{C_BB1, C_BB30}, {C_EE3, C_EE33}}, {2, 2}, -1, -1};
 // printed congruences of the paper (int64 coefficients, <= 33 sums)
 struct SmallTerm { int64_t a; uint32_t xn, xd, yn, yd; };
 struct SmallCong { char name[8]; int64_t L; uint32_t e, m, min_p, excluded_p; SmallTerm t[33]; };
@@ -49,8 +48,11 @@ struct GenTerm { uint32_t neg; uint64_t hi, lo; uint32_t xn, xd, yn, yd; };
 
 // generated-congruence tiers (name, test, threshold): names from congruences_gen.inc
 struct GenTier { const char *name; int test; uint64_t th; };
+// th = 0: not in the default schedule (BG_MID, p/34.3 with 305 sums, measured slower than BG_SML / BG_XL
+// everywhere); WV_TH_<name> enables or moves a tier.  The schedule uses, for each p,
+// the tier with the largest threshold <= p (sched_init sorts them).
 static GenTier kGenTiers[] = {
-    {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 1ull << 29}, {"BG_XL", 0, 1ull << 24}, {"BG_BIG", 0, 1ull << 30},
+    {"BG_SML", 0, 1ull << 17}, {"BG_MID", 0, 0}, {"BG_XL", 0, 1ull << 24}, {"BG_BIG", 0, 1ull << 30},
     {"EG_SML", 1, 1ull << 17}, {"EG_MID", 1, 1ull << 21}, {"EG_XL", 1, 1ull << 24}, {"EG_BIG", 1, 1ull << 30},
 };
 
@@ -111,19 +113,25 @@ static void sched_init(const Table &t) {
         snprintf(key, sizeof key, "WV_TH_%s", g.name);
         if (const char *e = getenv(key)) g.th = strtoull(e, nullptr, 0);
     }
-    for (const GenTier &g : kGenTiers) {
+    std::vector<GenTier> tiers(std::begin(kGenTiers), std::end(kGenTiers));
+    std::stable_sort(tiers.begin(), tiers.end(), [](const GenTier &a, const GenTier &b) { return a.th < b.th; });
+    for (const GenTier &g : tiers) {
         if (g.th == 0) continue;
         for (size_t i = NSMALL; i < t.hdr.size(); i++) {
             if (strncmp(t.hdr[i].name, g.name, 7) != 0) continue;
             int &n = g_sched.n[g.test];
-            if (n < 6) {
-                g_sched.th[g.test][n] = g.th;
-                g_sched.id[g.test][n] = (int)i;
-                n++;
+            if (n >= SCHED_TIERS) {   // cannot happen with the built-in table (static_assert below)
+                fprintf(stderr, "libwv: schedule holds %d tiers per test; %s dropped\n", SCHED_TIERS, g.name);
+                continue;
             }
+            if (g_sched.th[g.test][n - 1] >= g.th) continue;   // at or below an earlier threshold: dropped
+            g_sched.th[g.test][n] = g.th;
+            g_sched.id[g.test][n] = (int)i;
+            n++;
         }
     }
 }
+static_assert(sizeof kGenTiers / sizeof kGenTiers[0] / 2 + 2 <= SCHED_TIERS, "schedule tier capacity");
 
 // odd primes below 256: the bootstrap list that sieves [3, 65536)
 static const uint32_t h_boot[] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59, 61, 67,
@@ -174,7 +182,7 @@ static int set_err(int code, const char *fmt, ...) {
 // env vars WV_VARIANT0/1/2 (index into this table) for benchmarking; defaults below.
 typedef void (*ResKern)(const Rec *, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, ulonglong2 *,
                         unsigned long long *, uint32_t, const uint32_t *, uint32_t);
-typedef void (*LaneKern)(const Rec *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
+typedef void (*LaneKern)(const Rec *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t, uint64_t,
                          uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *, unsigned long long *);
 struct Variant { const char *name; int cls; ResKern fn; LaneKern lane; };
 static const Variant kVariants[] = {
@@ -345,6 +353,13 @@ static uint64_t ntiles(uint64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 1;
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static const uint64_t PART_BUDGET = 1ull << 24;   // partial pairs per batch (256 MiB)
+static const uint64_t PART_BUDGET_MIN = 1ull << 18;   // smallest WV_PART_BUDGET (tests: many batches)
+// partial pairs per batch for this call: PART_BUDGET, or the WV_PART_BUDGET knob (tests of the batching)
+static uint64_t part_budget() {
+    const char *e = getenv("WV_PART_BUDGET");
+    uint64_t b = e ? strtoull(e, nullptr, 0) : PART_BUDGET;
+    return b < PART_BUDGET_MIN ? PART_BUDGET_MIN : (b > PART_BUDGET ? PART_BUDGET : b);
+}
 
 enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2 /* 2 slots: first k with p >= 2^30, >= 2^44 */,
        M_CNT = 4 /* 3 slots: work counters per class */, M_NHITS = 7, M_CHECKSUM = 8, M_NBASE1 = 9,
@@ -374,7 +389,7 @@ static void layout_tail(Layout &L) {
     L.o_nch = o;   o += al(L.K * 8);
     L.o_start = o; o += al((L.K + 1) * 8);
     L.o_part = o;  o += al(PART_BUDGET * sizeof(ulonglong2));
-    L.o_kb = o;    o += al(2 * (L.K * CAP_CHUNKS / (PART_BUDGET / 2) + 4) * 8);
+    L.o_kb = o;    o += al(3 * (L.K * CAP_CHUNKS / (PART_BUDGET_MIN / 2) + 4) * 8);
     L.ngt = (L.prime_cap + 31) / 32 * L.ntests;
     L.o_gq = o;     o += al((L.ngt + 1) * 8);
     L.o_gstart = o; o += al((L.ngt + 1) * 8);
@@ -557,41 +572,31 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     }
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
     uint64_t hs[4], ht[3];
-    for (int attempt = 0; attempt < 2; attempt++) {
-        if (attempt == 1) {       // lane mode needs more partial pairs than one batch: redo in chunk mode
-            lane = false;
-            var0 = kChunkFallback0;
-            CK(cudaMemsetAsync(misc + M_ERR, 0, 8, st));
-            CK(cudaMemsetAsync(misc + M_FIRST64, 0xff, 16, st));
-            CK(cudaMemsetAsync(misc + M_TERMS, 0, 24, st));
+    if (K > 0) {
+        (void)table();
+        LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
+               nch, (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
+               (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr, segidx, L.segstride, LANE_SLICE,
+               LANE_QMAX, (lane && lane2) ? (unsigned long long *)(misc + M_LANE_T) : nullptr);
+        if (lane && lane2 && L.ngt > 0) {
+            const uint64_t nbw = (L.ngt * 32 + 255) / 256;
+            LAUNCH(lane_group_terms_kernel, (unsigned)(nbw < (uint64_t)c->sms * 16 ? nbw : c->sms * 16), 256, st,
+                   primes, n_dev, n_host, mode, g_sched, L.ngt, gq, (unsigned long long *)(misc + M_LANE_T));
+            const uint64_t nb = (L.ngt + 255) / 256;
+            LAUNCH(lane_slices_kernel, (unsigned)(nb < (uint64_t)c->sms * 8 ? nb : c->sms * 8), 256, st, gq, L.ngt,
+                   L.ntests, recs, K, nch, (const unsigned long long *)(misc + M_LANE_T), lane_items, 4096ull,
+                   LANE_QMAX);
         }
-        if (K > 0) {
-            (void)table();
-            LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
-                   nch, (unsigned long long *)(misc + M_FIRST64), (int *)(misc + M_ERR),
-                   (unsigned long long *)(misc + M_TERMS), lane ? gq : nullptr, segidx, L.segstride, LANE_SLICE,
-                   LANE_QMAX, (lane && lane2) ? (unsigned long long *)(misc + M_LANE_T) : nullptr);
-            if (lane && lane2 && L.ngt > 0) {
-                const uint64_t nbw = (L.ngt * 32 + 255) / 256;
-                LAUNCH(lane_group_terms_kernel, (unsigned)(nbw < (uint64_t)c->sms * 16 ? nbw : c->sms * 16), 256, st,
-                       primes, n_dev, n_host, mode, g_sched, L.ngt, gq, (unsigned long long *)(misc + M_LANE_T));
-                const uint64_t nb = (L.ngt + 255) / 256;
-                LAUNCH(lane_slices_kernel, (unsigned)(nb < (uint64_t)c->sms * 8 ? nb : c->sms * 8), 256, st, gq, L.ngt,
-                       L.ntests, recs, K, nch, (const unsigned long long *)(misc + M_LANE_T), lane_items, 4096ull,
-                       LANE_QMAX);
-            }
-        }
-        TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
-        if (lane) TRY(scan_excl<uint64_t>(gq, L.ngt, gstart, gstart + L.ngt, tiles, st));
-        LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
-        CK(cudaMemcpyAsync(ht, misc + M_TERMS, 24, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
-        if (lane) CK(cudaMemcpyAsync(&h[3], gstart + L.ngt, 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 32, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (!lane || h[2] <= PART_BUDGET) break;
     }
+    TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
+    if (lane) TRY(scan_excl<uint64_t>(gq, L.ngt, gstart, gstart + L.ngt, tiles, st));
+    LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
+    CK(cudaMemcpyAsync(ht, misc + M_TERMS, 24, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
+    if (lane) CK(cudaMemcpyAsync(&h[3], gstart + L.ngt, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 32, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     const uint64_t n = n_dev ? h[0] : n_host;
     if (n_primes_out) *n_primes_out = n;
     if ((int)h[1] != 0) return set_err(WV_EINVAL, "schedule chose a congruence not valid for some prime");
@@ -609,28 +614,36 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     // class boundaries (sorted input): items [0,gb[1]) class 0, [gb[1],gb[2]) class 1, [gb[2],G) class 2
     const uint64_t gb[4] = {0, sorted ? hs[0] : 0, sorted ? hs[2] : 0, G};
     const uint64_t kbd[4] = {0, sorted ? hs[1] : 0, sorted ? hs[3] : 0, K};
-    // batches of <= PART_BUDGET partial pairs, cut at record boundaries
-    std::vector<uint64_t> hk, hg;
-    if (G <= PART_BUDGET) {
+    // batches of <= budget partial pairs, cut at record boundaries (lane mode: at group boundaries, so each
+    // batch is whole lane items [hi_[b], hi_[b + 1]))
+    const uint64_t budget = part_budget();
+    std::vector<uint64_t> hk, hg, hi_;
+    if (G <= budget) {
         hk = {0, K};
         hg = {0, G};
+        hi_ = {0, h[3]};
     } else {
-        const uint64_t step = PART_BUDGET / 2;   // every record has <= CAP_CHUNKS << step chunks
+        // every record has <= CAP_CHUNKS chunks and every lane group <= 32 ntests LANE_QMAX slots, both << step
+        const uint64_t step = budget / 2;
         const uint64_t nb = (G + step - 1) / step;
-        LAUNCH(batch_bounds_kernel, (unsigned)((nb + 256) / 256), 256, st, start, K, step, nb, kb);
-        hk.resize(2 * (nb + 1));
-        CK(cudaMemcpyAsync(hk.data(), kb, 2 * (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+        LAUNCH(batch_bounds_kernel, (unsigned)((nb + 256) / 256), 256, st, start, K, step, nb, kb,
+               lane ? 32ull * L.ntests : 1ull, lane ? gstart : nullptr, L.ntests);
+        hk.resize(3 * (nb + 1));
+        CK(cudaMemcpyAsync(hk.data(), kb, (lane ? 3 : 2) * (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        hg.assign(hk.begin() + (nb + 1), hk.end());   // item bounds start[kb[b]]
+        hg.assign(hk.begin() + (nb + 1), hk.begin() + 2 * (nb + 1));   // partial-slot bounds start[kb[b]]
+        if (lane) hi_.assign(hk.begin() + 2 * (nb + 1), hk.end());    // lane-item bounds
         hk.resize(nb + 1);
     }
+    if (lane) CK(cudaMemsetAsync(misc + M_LANE_TERMS, 0, 8, st));   // the lane kernels' term counts, all batches
     for (size_t b = 0; b + 1 < hk.size(); b++) {
         const uint64_t klo = hk[b], khi = hk[b + 1], glo = hg[b], ghi = hg[b + 1];
         if (khi <= klo) continue;
         // 32-bit records: items [glo, min(ghi, g32)); 64-bit: [max(glo, g32), ghi)
         // per class: items [max(glo, gb[c]), min(ghi, gb[c+1])) of records [max(klo,kbd[c]), min(khi,kbd[c+1]));
         // unsorted input: every class kernel scans the whole batch and skips the other classes' records
-        if (lane && h[3] > 0) {     // lane mode for class 0 (single batch guaranteed above)
+        const uint64_t ia = lane ? hi_[b] : 0, ib = lane ? hi_[b + 1] : 0;
+        if (lane && ib > ia) {     // lane mode for class 0: this batch's lane items
             {   // WV_LANE_CHAIN (benchmarking / tests): chain mode per exponent / W step width, default 5
                 const char *ev = getenv("WV_LANE_CHAIN");
                 static uint32_t cur[64];
@@ -646,11 +659,10 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
                 }
             }
             CK(cudaMemsetAsync(misc + M_CNT, 0, 8, st));
-            CK(cudaMemsetAsync(misc + M_LANE_TERMS, 0, 8, st));
             EvPair ev{nullptr, nullptr, 0};
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
-            LAUNCH(kVariants[var0].lane, c->sms * c->occ[var0], RES_THREADS, st, recs, start, gstart, gq, L.ngt, h[3],
-                   L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT),
+            LAUNCH(kVariants[var0].lane, c->sms * c->occ[var0], RES_THREADS, st, recs, start, gstart, gq, L.ngt, ia,
+                   ib - ia, L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT),
                    lane2 ? (unsigned long long *)(misc + M_LANE_TERMS) : nullptr);
             if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }

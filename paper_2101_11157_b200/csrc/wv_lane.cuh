@@ -572,7 +572,7 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
     }
 }
 
-// items it in [0, nitems) processed largest-first (groups ascend in p); gstart = exclusive scan of
+// items it in [item_lo, item_lo + nitems) processed largest-first (groups ascend in p); gstart = exclusive scan of
 // gq (slices per group-test); start = per-record partial slots.
 // Step widths in chain mode (terms per step) for W (e = 3) and V (e = 2); build-time choices.
 #ifndef WV_LANE_KW
@@ -593,7 +593,7 @@ using RunV = std::conditional<WV_LANE_KV == 4, LaneRun2Q, LaneRunP<2, WV_LANE_KV
 __global__ void __launch_bounds__(RES_THREADS, WV_LANE2_MINB)
 residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                      const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
-                     uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
+                     uint64_t item_lo, uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
                      ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
                      unsigned long long *__restrict__ term_count) {
     const uint32_t chain_mask = c_lane_chain;          // bit 0: chain mode for e = 2, bit 1: for e = 3
@@ -603,7 +603,7 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
         if (lane == 0) it = atomicAdd(counter, 1ull);
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= nitems) break;
-        const uint64_t item = nitems - 1 - it;
+        const uint64_t item = item_lo + nitems - 1 - it;          // this batch's items [item_lo, item_lo + nitems)
         const uint64_t gt = find_rec(gstart, 0, ngt, item);
         const uint64_t q = item - gstart[gt], Q = gq[gt];
         const uint64_t g = gt / ntests, t = gt % ntests;

@@ -64,10 +64,11 @@ struct Rec {                // one (prime, test) pair; 32 bytes
     uint32_t test;          // 0 = W (B_{p-3}), 1 = V (E_{p-3})
 };
 
+constexpr int SCHED_TIERS = 10;
 struct Sched {              // tiered schedule + overrides
-    // test t (0 = W, 1 = V): use id[t][i] for the largest i with p >= th[t][i] (th[t][0] = 0)
-    uint64_t th[2][6];
-    int id[2][6];
+    // test t (0 = W, 1 = V): use id[t][i] for the largest i with p >= th[t][i]; th[t] ascends, th[t][0] = 0
+    uint64_t th[2][SCHED_TIERS];
+    int id[2][SCHED_TIERS];
     int n[2];
     int w_force, v_force;   // -1 = none
 };
@@ -92,10 +93,9 @@ __host__ __device__ __forceinline__ int schedule(const Sched &s, uint64_t p, int
     } else if (s.v_force >= 0) {
         return s.v_force;
     }
-    int id = s.id[test][0];
-    for (int i = 1; i < s.n[test]; i++)
-        if (p >= s.th[test][i]) id = s.id[test][i];
-    return id;
+    int i = s.n[test] - 1;                       // the largest threshold <= p (th ascending)
+    while (i > 0 && p < s.th[test][i]) i--;
+    return s.id[test][i];
 }
 
 __constant__ const double2 *c_termr;     // {fl(1/xd), fl(1/yd)} per term (same index as c_terms)
@@ -1035,13 +1035,13 @@ __device__ __forceinline__ void lane_slice_work(const M &mo, const ModD &md, con
     }
 }
 
-// items it in [0, nitems) processed largest-first (groups ascend in p);
+// items it in [item_lo, item_lo + nitems) processed largest-first (groups ascend in p);
 // gstart = exclusive scan of gq over group-tests; start = per-record partial slots.
 template <class M, int CLASS, int ENGINE>
 __global__ void __launch_bounds__(RES_THREADS)
 residue_lane_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                     const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
-                    uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
+                    uint64_t item_lo, uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
                     ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
                     unsigned long long *__restrict__ /*term_count: the plan counts this kernel's terms*/) {
     using W = typename M::W;
@@ -1051,7 +1051,7 @@ residue_lane_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ s
         if (lane == 0) it = atomicAdd(counter, 1ull);
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= nitems) break;
-        const uint64_t item = nitems - 1 - it;
+        const uint64_t item = item_lo + nitems - 1 - it;
         const uint64_t gt = find_rec(gstart, 0, ngt, item);
         const uint64_t q = item - gstart[gt], Q = gq[gt];
         const uint64_t g = gt / ntests, t = gt % ntests;
@@ -1218,19 +1218,34 @@ __global__ void split_kernel(const uint64_t *__restrict__ start, uint64_t K, con
 
 // For batch b (1 <= b < nb): record index kb[b] = largest k with start[k] <= b * step (k in [0, K]);
 // kb[nb + 1 + b] = start[kb[b]] (the batch's first item).
+// Batch b of the partial-pair buffer: records [kb[b], kb[b + 1]), partial slots from kb[nb + 1 + b]
+// (= start[kb[b]]).  Record boundaries are multiples of `align` (lane mode: whole groups of 32 primes x
+// ntests, so a lane item never straddles two batches) or K; with gstart (lane mode) kb[2 (nb + 1) + b]
+// is the first lane item of the batch (gstart at the boundary's group-test).
 __global__ void batch_bounds_kernel(const uint64_t *__restrict__ start, uint64_t K, uint64_t step, uint64_t nb,
-                                    uint64_t *__restrict__ kb) {
+                                    uint64_t *__restrict__ kb, uint64_t align, const uint64_t *__restrict__ gstart,
+                                    uint32_t ntests) {
+    const uint64_t ng = (K + align - 1) / align;                  // aligned boundaries g * align, g <= ng
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (uint64_t)gridDim.x * blockDim.x) {
-        if (b == 0) { kb[0] = 0; kb[nb + 1] = 0; continue; }
-        if (b == nb) { kb[b] = K; kb[nb + 1 + b] = start[K]; continue; }
-        const uint64_t target = b * step;
-        uint64_t lo = 0, hi = K + 1;
-        while (hi - lo > 1) {
-            uint64_t mid = (lo + hi) >> 1;
-            if (start[mid] <= target) lo = mid; else hi = mid;
+        uint64_t g;
+        if (b == 0) {
+            g = 0;
+        } else if (b == nb) {
+            g = ng;
+        } else {
+            const uint64_t target = b * step;
+            uint64_t lo = 0, hi = ng + 1;                          // largest g with start[min(g align, K)] <= target
+            while (hi - lo > 1) {
+                const uint64_t mid = (lo + hi) >> 1;
+                const uint64_t k = mid * align < K ? mid * align : K;
+                if (start[k] <= target) lo = mid; else hi = mid;
+            }
+            g = lo;
         }
-        kb[b] = lo;
-        kb[nb + 1 + b] = start[lo];
+        const uint64_t k = g * align < K ? g * align : K;
+        kb[b] = k;
+        kb[nb + 1 + b] = start[k];
+        if (gstart) kb[2 * (nb + 1) + b] = gstart[g * ntests];
     }
 }
 

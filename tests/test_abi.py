@@ -133,3 +133,17 @@ def test_left_factor_vanishes_exactly_where_excluded(pkg):
                 assert not vanishes, (c["name"], p)
     names = {c["name"]: c for c in pkg.congruences()}
     assert names["BB1"]["L"] % 7 == 0 and names["VOR12"]["L"] % 5 == 0 and names["EE33"]["L"] % 5 == 0
+
+
+def test_schedule_tier_boundaries(pkg):
+    """The default schedule takes, for each p, the tier with the largest threshold <= p (include/wv.h),
+    at every boundary (BG_MID is built but in no default range)."""
+    names = {c["id"]: c["name"] for c in pkg.congruences()}
+    W, V = pkg.MODE_W, pkg.MODE_V
+    want = [(W, 4095, "BB1"), (W, 4096, "BB30"), (W, (1 << 17) - 1, "BB30"), (W, 1 << 17, "BG_SML"),
+            (W, (1 << 24) - 1, "BG_SML"), (W, 1 << 24, "BG_XL"), (W, 1 << 29, "BG_XL"), (W, (1 << 30) - 1, "BG_XL"),
+            (W, 1 << 30, "BG_BIG"), (W, 1 << 44, "BG_BIG"),
+            (V, 4095, "EE3"), (V, 4096, "EE33"), (V, 1 << 17, "EG_SML"), (V, (1 << 21) - 1, "EG_SML"),
+            (V, 1 << 21, "EG_MID"), (V, 1 << 24, "EG_XL"), (V, (1 << 30) - 1, "EG_XL"), (V, 1 << 30, "EG_BIG")]
+    for test, p, name in want:
+        assert names[pkg.schedule(p, test)] == name, (test, p)

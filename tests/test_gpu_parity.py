@@ -252,13 +252,19 @@ def test_ragged_tail_64bit_window(wv):
     hits, res = wv.search(a, b, 3)
     ps = oracle.primes(a, b)
     assert res["p"].tolist() == ps
-    for r in res[sample_indices(len(res), 4)]:
-        p = int(r["p"])
-        assert int(r["res_w"]) == oracle.B_stafford_vandiver(p), p   # tier C (pinned in test_oracle_pins)
-        assert int(r["res_v"]) == oracle.E_quarter(p), p
+    sub = res[sample_indices(len(res), 4)]
+    rw, rv = _oracle_arrays([int(p) for p in sub["p"]], 3)         # tier B (definition-level), p < 2^32
+    _assert_equal(sub["p"], sub["res_w"], rw, "W above 2^30")
+    _assert_equal(sub["p"], sub["res_v"], rv, "V above 2^30")
     w = SUBWINDOWS["c4_head"]
     hits, res = wv.search(w.lo, w.hi, w.mode)
     assert res["p"].tolist() == oracle.primes(w.lo, w.hi)
+    # the C4 head's residues: every C4 oracle golden sample inside it (tier B, base-p digits)
+    gp, gw, gv, _ = _golden("c4")
+    inside = (gp >= w.lo) & (gp < w.hi)
+    assert inside.sum() >= 1
+    idx = np.searchsorted(res["p"], gp[inside])
+    _assert_equal(gp[inside], res["res_w"][idx], gw[inside], "C4 head W")
 
 
 def test_kernel_variants_bit_identical(wv):
@@ -312,11 +318,12 @@ def test_lane2_slicing_bit_exact(wv, items, monkeypatch):
 @pytest.mark.parametrize("chain", ["0", "1", "4"])
 def test_lane2_chain_modes_bit_exact(wv, chain, monkeypatch):
     """Chain mode (one table and one accumulator through adjacent sums, summation by parts) is on by default
-    (e = 2 and e = 3 four-term steps: WV_LANE_CHAIN = 5); no chains with W pair steps (0), e = 2 only (1)
-    and e = 3 only (4) must give the same residues on windows where
-    sums are a few terms long (BB30 / EE33 just above 4096: empty, one- and two-term sums) and on a
-    C2-size window, and agree with the oracle."""
-    windows = [(4000, 9000, 3), (5, 300000, 3), ((1 << 24) - 4000, (1 << 24) + 4000, 3)]
+    (e = 2 and e = 3 four-term steps: WV_LANE_CHAIN = 5); no chains with W pair steps (0), e = 2 only (1) and
+    e = 3 only (4) must give the same residues on windows where sums are a few terms long (BB30 / EE33 just
+    above 4096: empty, one- and two-term sums), on a C2-size window and on windows straddling 2^23 and the
+    tier bound 2^24, and agree with the oracle."""
+    windows = [(4000, 9000, 3), (5, 300000, 3), ((1 << 23) - 6000, (1 << 23) + 6000, 3),
+               ((1 << 24) - 4000, (1 << 24) + 4000, 3)]
     for lo, hi, mode in windows:
         _, ref = wv.search(lo, hi, mode)
         monkeypatch.setenv("WV_LANE_CHAIN", chain)
@@ -361,6 +368,10 @@ def test_fp64_tuple_steps_near_class_top(wv):
         wv.set_kernel_variant(1, ids["c1 fp s2/2"])
         sw, sv = wv.residues_of(ps, 3)
         assert tw.tolist() == sw.tolist() and tv.tolist() == sv.tolist()
+        # the 64-bit Montgomery engine (the class-2 arithmetic) on the same primes: IMAD pipe, not FP64
+        wv.set_kernel_variant(1, ids["c1 int s1/1"])
+        mw, mv = wv.residues_of(ps, 3)
+        assert mw.tolist() == tw.tolist() and mv.tolist() == tv.tolist()
         wv.set_kernel_variant(1, -1)
         wv.set_schedule_override(names["BB30"], names["EE33"])
         pw, pv = wv.residues_of(ps[2:], 3)
@@ -498,3 +509,54 @@ def test_frontier_window_primes_and_samples(wv):
     idx = np.searchsorted(got, gp[inside])
     _assert_equal(gp[inside], rw[idx], gw[inside], "frontier W")
     _assert_equal(gp[inside], rv[idx], gv[inside], "frontier V")
+
+
+
+def test_wv_search_symbol_and_enospc_two_call(wv):
+    """wv_search itself (not wv_search_shard): the two-call contract of include/wv.h -- too-small capacities
+    give WV_ENOSPC with *n_hits / *n_primes set to the sizes needed and nothing written; a second call with
+    those sizes succeeds and equals wv_search_shard; residues may be skipped (NULL, cap 0)."""
+    from paper_2101_11157_b200 import _wv
+    w = CONFIGS["c1"]
+    sh, sr, _ = wv.search_shard(w.lo, w.hi, w.mode, 0, 1, 0)
+    hits = np.zeros(1, dtype=_wv.HIT_DTYPE)
+    res = np.zeros(10, dtype=_wv.RES_DTYPE)
+    hits["p"] = 12345
+    rc, nh, npr = _wv.search_raw(w.lo, w.hi, w.mode, hits, res)
+    assert rc == _wv.WV_ENOSPC and (nh, npr) == (3, 9590)
+    assert int(hits["p"][0]) == 12345 and not res["p"].any()          # nothing written
+    hits = np.zeros(nh, dtype=_wv.HIT_DTYPE)
+    res = np.zeros(npr, dtype=_wv.RES_DTYPE)
+    rc, nh2, npr2 = _wv.search_raw(w.lo, w.hi, w.mode, hits, res)
+    assert rc == _wv.WV_OK and (nh2, npr2) == (nh, npr)
+    assert hits.tobytes() == sh.tobytes() and res.tobytes() == sr.tobytes()
+    rc, nh3, npr3 = _wv.search_raw(w.lo, w.hi, w.mode, hits, None)     # hits only
+    assert rc == _wv.WV_OK and nh3 == nh
+    gh, gr = wv.search(w.lo, w.hi, w.mode)                             # the binding's wv_search path
+    assert gh.tobytes() == sh.tobytes() and gr.tobytes() == sr.tobytes()
+    rc, _, _ = _wv.search_raw(10, 5, 3, hits, res)
+    assert rc == _wv.WV_EINVAL
+
+
+def test_lane_mode_batches_bit_exact(wv, monkeypatch):
+    """Lane mode cut into batches of the partial-pair buffer (group-aligned record ranges; the default
+    budget of 2^24 slots is only exceeded by windows of ~10^8 primes, so WV_PART_BUDGET = 2^18 forces
+    many batches here): C2 and a window straddling 2^30 (lane batches next to class-1 chunk items) give the
+    default bytes and checksums, and the lane kernels' term count is the unbatched one."""
+    for lo, hi, mode in [(5, 3 * 10 ** 6, 3), ((1 << 30) - 300000, (1 << 30) + 20000, 3)]:
+        ref = wv.DeviceSearch(lo, hi, mode).run()
+        r_res, r_chk = ref.res_np(), ref.checksum_int()
+        wv.stats_reset()
+        wv.stats_enable(True)
+        wv.DeviceSearch(lo, hi, mode).run()
+        t_ref = wv.stats()["terms32"]
+        monkeypatch.setenv("WV_PART_BUDGET", str(1 << 18))
+        wv.stats_reset()
+        got = wv.DeviceSearch(lo, hi, mode).run()
+        t_got = wv.stats()["terms32"]
+        wv.stats_enable(False)
+        monkeypatch.delenv("WV_PART_BUDGET")
+        g_res = got.res_np()
+        assert got.n_primes == ref.n_primes
+        assert g_res[0].tobytes() == r_res[0].tobytes() and g_res[1].tobytes() == r_res[1].tobytes(), (lo, hi)
+        assert got.checksum_int() == r_chk and t_got == t_ref
