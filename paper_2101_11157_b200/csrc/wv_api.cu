@@ -207,12 +207,20 @@ static const Variant kVariants[] = {
     // 8/7 578/365, 10/6 560/379 (register spills beyond 6/6) (term-by-term: 880/552)
     {"c1 fp tuples 4/4", 1, residue_kernel<Mont64, 1, 1, 4, 4, true>, nullptr},
     {"c1 fp tuples 6/6", 1, residue_kernel<Mont64, 1, 1, 6, 6, true>, nullptr},
+    // Mont64 K-term steps with lazy tables (class 2, sum-aligned congruences); also selectable for class 1
+    {"c2 int tuples 4/4", 2, residue_kernel<Mont64, 2, 0, 4, 4, true>, nullptr},   // 18
+    {"c2 int tuples 6/6", 2, residue_kernel<Mont64, 2, 0, 6, 6, true>, nullptr},
+    {"c2 int tuples 8/8", 2, residue_kernel<Mont64, 2, 0, 8, 8, true>, nullptr},   // 20 (class-2 default)
+    {"c2 int tuples 8/6", 2, residue_kernel<Mont64, 2, 0, 8, 6, true>, nullptr},
+    {"c1 int tuples 4/4", 1, residue_kernel<Mont64, 2, 0, 4, 4, true>, nullptr},
 
 };
 static const int NVAR = sizeof kVariants / sizeof kVariants[0];
 static_assert(NVAR <= 32, "DevCtx::occ holds 32 variants");
-static const int kDefaultVariant[3] = {15, 17, 8};  // measured best (scripts/variant_sweep.py)
-static int g_variant[3] = {15, 17, 8};              // per class
+// measured best (scripts/variant_sweep.py; class 2: scripts/class2_timing.py, first primes above 2^44, W+V:
+// s1/1 2.48e11, tuples 4/4 4.72e11, 6/6 6.10e11, 8/6 6.65e11, 8/8 7.09e11 terms/s)
+static const int kDefaultVariant[3] = {15, 17, 20};
+static int g_variant[3] = {15, 17, 20};             // per class
 static const int kChunkFallback0 = 13;             // class-0 chunk variant when lane mode is unusable
 static void read_variant_env() {
     static bool done = false;

@@ -22,6 +22,7 @@
 //     X = C1 * (C0 * L)^{-1}  mod p.
 #pragma once
 #include <stdint.h>
+#include <type_traits>
 #include "wv_mont.cuh"
 #include "wv_scan.cuh"
 
@@ -657,6 +658,147 @@ __device__ __forceinline__ void fp_tuple_work(const M &mo, const ModD &md, uint6
     }
 }
 
+// ---------------------------------------------------------------- class 2: Mont64 K-term steps
+// The same K-term step as RunDK (a1 <- a1 D + a0 N, a0 <- a0 D; D, N polynomials of degree Ke, (K-1)e in s
+// advanced by step-K forward differences) in 64-bit Montgomery arithmetic (R = 2^64, p < 2^62), for the
+// primes no narrower engine covers (p >= 2^44).  A 64-bit product costs ~20 IMAD-class instructions
+// (32-bit limbs), so the tables are *lazy*: plain 64-bit additions (two instructions, no compare /
+// select) and a Barrett reduction of every entry to [0, 2p) at most rb steps apart, rb = 63 - bitlen(p)
+// (capped at 16): after n unreduced steps an entry is a binomial-weighted sum of entries < 2p, so it is
+// < 2p 2^n <= 2^64.  Only D_0 and N_0 enter products, through mulr (b may be any 64-bit value).
+template <int E, int K>
+struct RunMK {
+    static constexpr int DD = K * E, DN = (K - 1) * E;
+    uint64_t D[DD + 1], N[DN + 1], a0, a1;
+    static __device__ __forceinline__ uint64_t red2(const Mont64 &mo, uint64_t t) {   // [0, 3p) -> [0, 2p)
+        return t >= mo.p2 ? t - mo.p2 : t;
+    }
+    // a b R^{-1} for a < 2p and any 64-bit b: (a b + m p) / R < 2p + p, one conditional subtract
+    static __device__ __forceinline__ uint64_t mulr(const Mont64 &mo, uint64_t a, uint64_t b) {
+        return red2(mo, mo.mul(a, b));
+    }
+    static __device__ __forceinline__ uint64_t sub(const Mont64 &mo, uint64_t a, uint64_t b) {  // [0, 2p)
+        const uint64_t s = a + mo.p2 - b;                                                       // (0, 4p)
+        return s >= mo.p2 ? s - mo.p2 : s;
+    }
+    // x < 2^64 -> [0, 2p), same residue: q = hi(x mu), mu = floor(2^64 / p), is floor(x / p) or one less
+    static __device__ __forceinline__ uint64_t bred(const Mont64 &mo, uint64_t mu, uint64_t x) {
+        return x - __umul64hi(x, mu) * mo.p;
+    }
+    __device__ __forceinline__ void setup(const Mont64 &mo, uint64_t x) {   // x < p
+        const uint64_t xt = mo.to(x), xx = mo.mul(xt, xt);
+        uint64_t u, d1, d2, d3 = 0;
+        if (E == 3) {
+            const uint64_t r3 = mo.add(mo.add(mo.r1, mo.r1), mo.r1), x3 = mo.add(mo.add(xt, xt), xt);
+            u = mo.mul(xx, xt);                                                // x^3
+            d1 = mo.add(mo.add(mo.add(xx, xx), xx), mo.add(x3, mo.r1));        // 3x^2 + 3x + 1
+            d3 = mo.add(r3, r3);                                               // 6
+            d2 = mo.add(mo.add(x3, x3), d3);                                   // 6x + 6
+        } else {
+            u = xx;                                                            // x^2
+            d1 = mo.add(mo.add(xt, xt), mo.r1);                                // 2x + 1
+            d2 = mo.add(mo.r1, mo.r1);                                         // 2
+        }
+        #pragma unroll
+        for (int i = 0; i <= DD; i++) {
+            uint64_t q[K], pre[K + 1], suf[K + 1];
+            #pragma unroll
+            for (int k = 0; k < K; k++) {
+                q[k] = u;
+                u = mo.add(u, d1);
+                d1 = mo.add(d1, d2);
+                if (E == 3) d2 = mo.add(d2, d3);
+            }
+            pre[1] = q[0];
+            #pragma unroll
+            for (int k = 1; k < K; k++) pre[k + 1] = mo.mul(pre[k], q[k]);
+            D[i] = pre[K];
+            if (i <= DN) {
+                suf[K - 1] = q[K - 1];
+                #pragma unroll
+                for (int k = K - 2; k >= 1; k--) suf[k] = mo.mul(suf[k + 1], q[k]);
+                uint64_t n = mo.add(suf[1], pre[K - 1]);                       // prod_{j != 0} + prod_{j != K-1}
+                #pragma unroll
+                for (int k = 1; k < K - 1; k++) n = mo.add(n, mo.mul(pre[k], suf[k + 1]));
+                N[i] = n;
+            }
+        }
+        #pragma unroll
+        for (int k = 1; k <= DD; k++) {
+            #pragma unroll
+            for (int i = DD; i >= k; i--) D[i] = sub(mo, D[i], D[i - 1]);
+        }
+        #pragma unroll
+        for (int k = 1; k <= DN; k++) {
+            #pragma unroll
+            for (int i = DN; i >= k; i--) N[i] = sub(mo, N[i], N[i - 1]);
+        }
+        a0 = mo.r1;
+        a1 = 0;
+    }
+    template <bool MASK>
+    __device__ __forceinline__ void step(const Mont64 &mo, bool act) {
+        const uint64_t n1 = mo.add(mulr(mo, a1, D[0]), mulr(mo, a0, N[0]));
+        const uint64_t n0 = mulr(mo, a0, D[0]);
+        a1 = (!MASK || act) ? n1 : a1;
+        a0 = (!MASK || act) ? n0 : a0;
+        #pragma unroll
+        for (int i = 0; i < DD; i++) D[i] += D[i + 1];
+        #pragma unroll
+        for (int i = 0; i < DN; i++) N[i] += N[i + 1];
+    }
+    __device__ __forceinline__ void reduce(const Mont64 &mo, uint64_t mu) {
+        #pragma unroll
+        for (int i = 0; i < DD; i++) D[i] = bred(mo, mu, D[i]);
+        #pragma unroll
+        for (int i = 0; i < DN; i++) N[i] = bred(mo, mu, N[i]);
+    }
+    __device__ __forceinline__ void single(const Mont64 &mo, uint64_t x, bool act) {   // one term s = x
+        const uint64_t xt = mo.to(x), x2 = mo.mul(xt, xt);
+        const uint64_t w = E == 3 ? mo.mul(x2, xt) : x2;
+        const uint64_t n1 = mo.add(mo.mul(a1, w), a0);
+        const uint64_t n0 = mo.mul(a0, w);
+        a1 = act ? n1 : a1;
+        a0 = act ? n0 : a0;
+    }
+};
+
+// lane's run [x0, x0 + n) of one sum with Mont64 K-term steps, folded with a_j and merged into (C0, C1)
+template <int E, int K>
+__device__ __forceinline__ void int_tuple_work(const Mont64 &mo, uint64_t p, uint64_t x0, uint64_t n, uint64_t coef_m,
+                                               uint64_t &C0, uint64_t &C1) {
+    const uint64_t ns = n / K, rem = n - K * ns;
+    const bool act = n != 0;
+    const uint64_t kmin = __reduce_min_sync(0xffffffffu, act ? (uint32_t)ns : 0xffffffffu);
+    if (kmin == 0xffffffffu) return;
+    const uint64_t kmax = __reduce_max_sync(0xffffffffu, act ? (uint32_t)ns : 0u);
+    const uint32_t rmax = __reduce_max_sync(0xffffffffu, (uint32_t)rem);
+    const int bl = 64 - __clzll(p);
+    const uint32_t rb = __reduce_min_sync(0xffffffffu, bl >= 62 ? 1u : (63 - bl > 16 ? 16u : (uint32_t)(63 - bl)));
+    const uint64_t mu = ~0ull / p;                                            // floor((2^64 - 1) / p) = floor(2^64 / p)
+    RunMK<E, K> run;
+    run.setup(mo, act ? x0 : 1);
+    uint32_t since = 0;
+    uint64_t i = 0;
+    #pragma unroll 1
+    for (; i < kmin; i++) {
+        run.template step<false>(mo, true);
+        if (++since == rb) { run.reduce(mo, mu); since = 0; }
+    }
+    #pragma unroll 1
+    for (; i < kmax; i++) {
+        run.template step<true>(mo, i < ns);
+        if (++since == rb) { run.reduce(mo, mu); since = 0; }
+    }
+    for (uint32_t r = 0; r < rmax; r++) run.single(mo, x0 + K * ns + r, r < rem);
+    if (act) {
+        const uint64_t c1 = mo.mul(run.a1, coef_m);                          // fold a_j
+        const uint64_t n1 = mo.add(mo.mul(C0, c1), mo.mul(C1, run.a0));      // eqnCombinePairs
+        C0 = mo.mul(C0, run.a0);
+        C1 = n1;
+    }
+}
+
 template <class M>
 __device__ __forceinline__ void combine(const M &mo, typename M::W &C0, typename M::W &C1,
                                         typename M::W c0, typename M::W c1) {
@@ -830,7 +972,12 @@ template <class M, int CLASS, int ENGINE, int S2, int S3, bool PAIRS = false>
 #ifndef WV_FPT_MINB
 #define WV_FPT_MINB 2       // FP64 K-term kernels: resident blocks per SM targeted by register allocation
 #endif
-__global__ void __launch_bounds__(RES_THREADS, (ENGINE == 0 && CLASS == 0) ? 1 : ((ENGINE == 1 && PAIRS) ? WV_FPT_MINB : 3))
+#ifndef WV_IT_MINB
+#define WV_IT_MINB 2        // Mont64 K-term kernels: resident blocks per SM targeted by register allocation
+#endif
+__global__ void __launch_bounds__(RES_THREADS, (ENGINE == 0 && CLASS == 0) ? 1
+                                              : ((ENGINE == 1 && PAIRS) ? WV_FPT_MINB
+                                              : ((ENGINE == 0 && PAIRS && (S2 > 1 || S3 > 1)) ? WV_IT_MINB : 3)))
 residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start, uint64_t klo, uint64_t khi,
                uint64_t g_lo, uint64_t g_hi, uint64_t part_base, ulonglong2 *__restrict__ partials,
                unsigned long long *__restrict__ counter, uint32_t class_mask,
@@ -939,7 +1086,17 @@ residue_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
             if (lane == 0) tab.cont = 0;
             __syncwarp();
         }
-        if (ENGINE == 1 && PAIRS && cg.seg) {                // four-term FP64 steps over the lane's run
+        bool tuples = false;
+        if constexpr (ENGINE == 0 && PAIRS && (S2 > 1 || S3 > 1) && std::is_same<M, Mont64>::value) {
+            if (cg.seg) {                                    // Mont64 K-term steps over the lane's run (class 2)
+                const uint64_t x0 = tab.first[0] + t0, nl = t1 > t0 ? t1 - t0 : 0;
+                if (cg.e == 3) int_tuple_work<3, (S3 > 1 ? S3 : 2)>(mo, r.p, x0, nl, tab.coef[0], C0, C1);
+                else int_tuple_work<2, (S2 > 1 ? S2 : 2)>(mo, r.p, x0, nl, tab.coef[0], C0, C1);
+                tuples = true;
+            }
+        }
+        if (tuples) {
+        } else if (ENGINE == 1 && PAIRS && cg.seg) {                // four-term FP64 steps over the lane's run
             md.init(r.p);
             const uint64_t x0 = tab.first[0] + t0, nl = t1 > t0 ? t1 - t0 : 0;
             // tuple widths: S2 / S3 reinterpreted as K for e = 2 / e = 3 (at least 2)

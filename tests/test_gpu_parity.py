@@ -352,6 +352,18 @@ def test_class2_64bit_montgomery_cross_congruence(wv):
         wv.set_schedule_override(-1, -1)
     assert out["BB1"] == out["BB30"]
     assert 0 <= out["BB1"][0] < p and 0 <= out["BB1"][1] < p
+    # the default class-2 engine (Mont64 eight-term steps with lazy tables, BG_BIG / EG_BIG) against the
+    # term-by-term Mont64 engine, on the default schedule, for two primes above 2^44
+    ids = {name: vid for vid, name, cls in wv.kernel_variants()}
+    ps = [p, 17592186044437]                  # the two smallest primes above 2^44
+    dw, dv = wv.residues_of(ps, 3)
+    try:
+        wv.set_kernel_variant(2, ids["c2 int s1/1"])
+        sw, sv = wv.residues_of(ps, 3)
+    finally:
+        wv.set_kernel_variant(2, -1)
+    assert dw.tolist() == sw.tolist() and dv.tolist() == sv.tolist()
+    assert (int(dw[0]), int(dv[0])) == out["BB1"]
 
 
 def test_fp64_tuple_steps_near_class_top(wv):
