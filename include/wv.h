@@ -116,9 +116,12 @@ int wv_device_workspace_bytes(uint64_t lo, uint64_t hi, uint32_t mode,
  *   d_workspace           >= wv_device_workspace_bytes(...) bytes, 256-byte aligned
  *                         (NULL: the library allocates it stream-ordered);
  *   stream                a cudaStream_t (NULL = legacy default stream).
- * On return, *n_primes and *n_hits (host) hold the counts; the stream has been
- * synchronised (the counts are needed on the host).  Returns WV_ENOSPC if
- * prime_cap or workspace_bytes is too small (nothing written). */
+ * On return, *n_primes (host) holds the prime count (known after the plan step;
+ * the call waits once for it).  With n_hits != NULL, *n_hits holds the hit count
+ * and the stream has been synchronised; with n_hits == NULL the call returns as
+ * soon as the last kernel is enqueued (hits, residues and checksum are complete
+ * when the stream reaches that point; the hit count is not reported).  Returns
+ * WV_ENOSPC if prime_cap or workspace_bytes is too small (nothing written). */
 int wv_search_device(uint64_t lo, uint64_t hi, uint32_t mode,
                      uint32_t shard, uint32_t nshards, uint64_t block,
                      uint64_t *d_primes, uint64_t *d_res_w, uint64_t *d_res_v,

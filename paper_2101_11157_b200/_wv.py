@@ -222,7 +222,9 @@ class DeviceSearch:
         self.n_primes = 0
         self.n_hits = 0
 
-    def run(self, stream=None):
+    def run(self, stream=None, hit_count=True):
+        """One wv_search_device call.  hit_count=False: do not wait for the hit count (the call returns once
+        the work is enqueued; n_hits is then None until a run with hit_count=True)."""
         import torch
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         npr, nh = ctypes.c_size_t(), ctypes.c_size_t()
@@ -230,8 +232,9 @@ class DeviceSearch:
         _check(lib().wv_search_device(lo, hi, mode, shard, nshards, block, _ptr(self.primes), _ptr(self.res_w),
                                       _ptr(self.res_v), _ptr(self.hits), _ptr(self.checksum), self.cap,
                                       _ptr(self.workspace), self.ws_bytes, ctypes.c_void_p(st.cuda_stream),
-                                      ctypes.byref(npr), ctypes.byref(nh)))
-        self.n_primes, self.n_hits = int(npr.value), int(nh.value)
+                                      ctypes.byref(npr), ctypes.byref(nh) if hit_count else None))
+        self.n_primes = int(npr.value)
+        self.n_hits = int(nh.value) if hit_count else None
         return self
 
     # host views (copies) of the outputs

@@ -7,6 +7,7 @@
 // kernels of wv_sieve.cuh / wv_residue.cuh.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <nvtx3/nvToolsExt.h>   // NVTX v3, header-only: ranges cost nothing unless a profiler is attached
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -139,6 +140,14 @@ static const uint32_t h_boot[] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 4
                                   149, 151, 157, 163, 167, 173, 179, 181, 191, 193, 197, 199, 211, 223,
                                   227, 229, 233, 239, 241, 251};
 static const uint64_t BASE0_HI = 65536;
+
+// ------------------------------------------------------------------ NVTX ranges (nsys / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
@@ -555,6 +564,7 @@ static int base_list(DevCtx *c, const Layout &L, void *ws, cudaStream_t st, cons
 static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev, uint64_t n_host, uint64_t K,
                         uint32_t mode, bool sorted, uint64_t *res_w, uint64_t *res_v, void *ws, const Layout &L,
                         cudaStream_t st, uint64_t *n_primes_out) {
+    NvtxRange range("a2-a5 plan, residues, finalize");
     uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
     Rec *recs = (Rec *)WS(ws, L.o_recs);
     uint64_t *nch = (uint64_t *)WS(ws, L.o_nch);
@@ -740,6 +750,7 @@ extern "C" int wv_device_workspace_bytes(uint64_t lo, uint64_t hi, uint32_t mode
 static int search_device_impl(const Layout &L, uint64_t *d_primes, uint64_t *d_res_w, uint64_t *d_res_v,
                               wv_hit *d_hits, uint64_t *d_checksum, void *ws, cudaStream_t st, size_t *n_primes,
                               size_t *n_hits) {
+    NvtxRange range("wv_search_device");
     DevCtx *c;
     TRY(ctx_get(&c));
     uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
@@ -748,10 +759,14 @@ static int search_device_impl(const Layout &L, uint64_t *d_primes, uint64_t *d_r
     const uint32_t *base;
     uint32_t nbh;
     const uint64_t *nbd;
-    TRY(base_list(c, L, ws, st, &base, &nbh, &nbd));
-    TRY(run_sieve<uint64_t>(L.map, L.nseg, base, nbh, nbd, d_primes, L.prime_cap, misc + M_NPRIMES, ws, L, st));
+    {
+        NvtxRange r1("a1 sieve");
+        TRY(base_list(c, L, ws, st, &base, &nbh, &nbd));
+        TRY(run_sieve<uint64_t>(L.map, L.nseg, base, nbh, nbd, d_primes, L.prime_cap, misc + M_NPRIMES, ws, L, st));
+    }
     uint64_t n = 0;
     TRY(run_residues(c, d_primes, misc + M_NPRIMES, 0, L.K, L.mode, true, d_res_w, d_res_v, ws, L, st, &n));
+    NvtxRange r6("a6 flags, hits, checksum");
     if (n > L.prime_cap) return set_err(WV_ENOSPC, "prime count %llu exceeds bound %llu", (unsigned long long)n,
                                         (unsigned long long)L.prime_cap);
     // residues not requested -> WV_RES_NONE; hit flags; checksum
@@ -769,11 +784,13 @@ static int search_device_impl(const Layout &L, uint64_t *d_primes, uint64_t *d_r
                    (HitOut *)d_hits);
     }
     if (d_checksum) CK(cudaMemcpyAsync(d_checksum, misc + M_CHECKSUM, 8, cudaMemcpyDeviceToDevice, st));
-    uint64_t nh = 0;
-    CK(cudaMemcpyAsync(&nh, misc + M_NHITS, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
     if (n_primes) *n_primes = n;
-    if (n_hits) *n_hits = nh;
+    if (n_hits) {                      // the hit count is wanted on the host: wait for it
+        uint64_t nh = 0;
+        CK(cudaMemcpyAsync(&nh, misc + M_NHITS, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        *n_hits = nh;
+    }
     return WV_OK;
 }
 

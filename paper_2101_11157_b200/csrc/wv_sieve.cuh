@@ -10,8 +10,8 @@
 // Marking, per segment:
 //   phase 1  q in {3..31}: each thread builds whole 32-bit words from the
 //            residue n mod q (no atomics);
-//   phase 2  37 <= q < 2048: all threads stride over the multiples of one q
-//            (shared-memory atomicOr), q after q;
+//   phase 2  37 <= q < 2048: one warp per q, its lanes stride over the multiples
+//            (shared-memory atomicOr), the warps on different q;
 //   phase 3  q >= 2048: one thread per prime.
 // Marks start at max(q^2, first odd multiple >= segment start), so base primes
 // inside the window survive.  Then count (per-segment totals -> scan) and a
@@ -102,22 +102,28 @@ sieve_segments_kernel(SegMap map, const uint32_t *__restrict__ base, uint32_t nb
     }
     __syncthreads();
 
-    // phase 2: medium primes, all threads on one q at a time
-    uint32_t j = 10;                              // base[] = 3,5,7,...: entries 0..9 are <= 31
-    for (; j < nbase; j++) {
-        const uint32_t q = base[j];
-        if (q >= SIEVE_MED) break;
+    // phase 2: medium primes, one warp per q (warps take q_j, q_{j+8}, ...), lanes stride over its multiples;
+    // the per-q start offset (a 64-bit division) is computed by one warp instead of serially by all threads
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    uint32_t j3 = 10, hi3 = nbase;                // j3 = first index with base[j3] >= SIEVE_MED (ascending)
+    while (j3 < hi3) {
+        const uint32_t mid = (j3 + hi3) >> 1;
+        if (base[mid] < SIEVE_MED) j3 = mid + 1; else hi3 = mid;
+    }
+    const uint64_t lim = (ne - n0 + 1) >> 1;      // bit indices < lim are in range
+    for (uint32_t jj = 10 + warp; jj < j3; jj += nwarps) {   // base[] = 3,5,7,...: entries 0..9 are <= 31
+        const uint32_t q = base[jj];
         const uint64_t qq = (uint64_t)q * q;
-        if (qq >= ne) { j = nbase; break; }
+        if (qq >= ne) break;                      // ascending: later q of this warp are larger
         uint64_t st = n0 > qq ? n0 : qq;
         uint64_t m = (st + q - 1) / q * q;
         if (!(m & 1)) m += q;
         if (m >= ne) continue;
         const uint64_t i0 = (m - n0) >> 1;
-        const uint64_t lim = (ne - n0 + 1) >> 1;   // bit indices < lim are in range
-        for (uint64_t i = i0 + (uint64_t)threadIdx.x * q; i < lim; i += (uint64_t)blockDim.x * q)
+        for (uint64_t i = i0 + (uint64_t)lane * q; i < lim; i += 32ull * q)
             atomicOr(&comp[i >> 5], 1u << (i & 31));
     }
+    const uint32_t j = j3;
     // phase 3: large primes, one thread each
     for (uint32_t k = j + threadIdx.x; k < nbase; k += blockDim.x) {
         const uint32_t q = base[k];
@@ -126,7 +132,6 @@ sieve_segments_kernel(SegMap map, const uint32_t *__restrict__ base, uint32_t nb
         uint64_t st = n0 > qq ? n0 : qq;
         uint64_t m = (st + q - 1) / q * q;
         if (!(m & 1)) m += q;
-        const uint64_t lim = (ne - n0 + 1) >> 1;
         for (uint64_t i = (m - n0) >> 1; i < lim; i += q) atomicOr(&comp[i >> 5], 1u << (i & 31));
     }
     __syncthreads();

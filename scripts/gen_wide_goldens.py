@@ -32,6 +32,7 @@ import oracle  # noqa: E402
 from paper_2101_11157_b200.workloads import CONFIGS, sample_indices  # noqa: E402
 
 CACHE = os.path.join(ROOT, "scripts", "data", "oracle_wide_cache.jsonl")
+CACHE_GLOB = os.path.join(ROOT, "scripts", "data", "oracle_wide_cache*.jsonl")   # + other hosts' shares
 GOLD = os.path.join(ROOT, "tests", "golden")
 NONE = (1 << 64) - 1
 K = 64
@@ -73,9 +74,10 @@ def _work(task):
 
 
 def _cache():
+    import glob
     done = {}
-    if os.path.exists(CACHE):
-        with open(CACHE) as f:
+    for path in sorted(glob.glob(CACHE_GLOB)):
+        with open(path) as f:
             for line in f:
                 if line.strip():
                     d = json.loads(line)
@@ -83,14 +85,28 @@ def _cache():
     return done
 
 
-def run(workers):
+def run(workers, reverse=False, limit=None, out=CACHE, deadline=None):
+    """Compute the missing tasks (in order, or from the end with reverse -- a second host's share);
+    limit: at most that many tasks; deadline: seconds after which no further task starts."""
     done = _cache()
     todo = [t for t in _tasks() if (t[1], t[2]) not in done]
+    if reverse:
+        todo = todo[::-1]
+    if limit is not None:
+        todo = todo[:limit]
     print(f"{len(done)} cached, {len(todo)} to do, {workers} workers", flush=True)
+    t_start = time.time()
     ctx = multiprocessing.get_context("spawn")
-    with ProcessPoolExecutor(max_workers=workers, mp_context=ctx) as ex, open(CACHE, "a") as f:
-        futs = [ex.submit(_work, t) for t in todo]
-        for fu in as_completed(futs):
+    with ProcessPoolExecutor(max_workers=workers, mp_context=ctx) as ex, open(out, "a") as f:
+        futs = []
+        pending = list(todo)
+        while pending and len(futs) < workers:
+            futs.append(ex.submit(_work, pending.pop(0)))
+        while futs:
+            fu = next(as_completed(futs))
+            futs.remove(fu)
+            if pending and (deadline is None or time.time() - t_start < deadline):
+                futs.append(ex.submit(_work, pending.pop(0)))
             tag, p, test, r, dt = fu.result()
             f.write(json.dumps(dict(tag=tag, p=p, test=test, res=r, seconds=round(dt, 1),
                                     tier="B (sum k^-2 mod p^2, base-p digits)" if test == "W"
@@ -135,9 +151,13 @@ def main():
     ap.add_argument("cmd", choices=["run", "assemble"])
     ap.add_argument("--workers", type=int, default=os.cpu_count())
     ap.add_argument("--partial", action="store_true")
+    ap.add_argument("--reverse", action="store_true")
+    ap.add_argument("--limit", type=int, default=None)
+    ap.add_argument("--deadline", type=float, default=None)
+    ap.add_argument("--out", default=CACHE)
     a = ap.parse_args()
     if a.cmd == "run":
-        run(a.workers)
+        run(a.workers, a.reverse, a.limit, a.out, a.deadline)
     else:
         assemble(a.partial)
 

@@ -29,7 +29,56 @@ KEYS = [
 ]
 
 
+MUL_OPS = ("IMAD.WIDE", "IMAD.HI", "IMAD", "IMUL")     # integer multiplies (IMAD.IADD / IMAD.MOV / IMAD.X excluded)
+STALLS = ("math", "not_selected", "selected", "wait", "dispatch", "no_inst", "short_sb", "long_sb", "mio",
+          "branch_resolving")
+
+
+def opcode_mix(path):
+    """Executed SASS instructions per opcode (ncu source page) and stall-sample shares of the first kernel."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return None, None
+    hdr = rows[1]
+    H = {h: i for i, h in enumerate(hdr)}
+    ex, st = collections.Counter(), collections.Counter()
+    for r in rows[2:]:
+        if len(r) < len(hdr):
+            continue
+        w = r[H["Source"]].split()
+        if not w:
+            continue
+        op = w[1] if w[0].startswith("@") else w[0]
+        ex[op] += int(r[H["Instructions Executed"]] or 0)
+        for k in STALLS:
+            col = "stall_" + k
+            if col in H:
+                st[k] += int(r[H[col]] or 0)
+    return ex, st
+
+
+def mul_share(ex):
+    tot = sum(ex.values())
+    mul = sum(c for op, c in ex.items() if op in ("IMAD", "IMUL") or op.startswith(("IMAD.WIDE", "IMAD.HI")))
+    return mul, tot
+
+
 def rep(path):
+    ex, st = opcode_mix(path)
+    _rep_raw(path)
+    if ex:
+        mul, tot = mul_share(ex)
+        print(f"  {'warp instructions executed':32s} {tot}")
+        print(f"  {'mul opcode share':32s} {mul / tot:.4f} (IMAD, IMAD.WIDE, IMAD.HI, IMUL of all executed SASS)")
+        print("  opcode mix: " + ", ".join(f"{op} {c / tot:.3f}" for op, c in ex.most_common(12)))
+        stot = sum(st.values())
+        if stot:
+            print("  stall samples: " + ", ".join(f"{k} {v / stot:.2f}" for k, v in st.most_common(8)))
+
+
+def _rep_raw(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
