@@ -192,7 +192,8 @@ static int set_err(int code, const char *fmt, ...) {
 typedef void (*ResKern)(const Rec *, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, ulonglong2 *,
                         unsigned long long *, uint32_t, const uint32_t *, uint32_t);
 typedef void (*LaneKern)(const Rec *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t, uint64_t,
-                         uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *, unsigned long long *);
+                         uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *, unsigned long long *,
+                         uint32_t);
 struct Variant { const char *name; int cls; ResKern fn; LaneKern lane; };
 static const Variant kVariants[] = {
     {"c0 int s1/1", 0, residue_kernel<Mont32, 0, 0, 1, 1>, nullptr},
@@ -381,7 +382,8 @@ static uint64_t part_budget() {
 enum { M_NPRIMES = 0, M_ERR = 1, M_FIRST64 = 2 /* 2 slots: first k with p >= 2^30, >= 2^44 */,
        M_CNT = 4 /* 3 slots: work counters per class */, M_NHITS = 7, M_CHECKSUM = 8, M_NBASE1 = 9,
        M_SPLIT = 10 /* 4 slots */, M_TERMS = 14 /* 3 slots: terms per class */, M_LANE_T = 17,
-       M_LANE_TERMS = 18 /* terms executed by the lane-mode v2 kernel (counted there) */, M_SLOTS = 24 };
+       M_LANE_TERMS = 18 /* terms executed by the lane-mode v2 kernel (counted there) */,
+       M_LANE_SLICED = 19 /* 2 slots: lane group-tests with Q > 1, all lane group-tests */, M_SLOTS = 24 };
 
 struct Layout {
     // problem
@@ -589,7 +591,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         lane_items = (ev ? atof(ev) : 2.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
     }
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
-    uint64_t hs[4], ht[3];
+    uint64_t hs[4], ht[3], hsl[2] = {0, 0};
     if (K > 0) {
         (void)table();
         LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
@@ -600,10 +602,10 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             const uint64_t nbw = (L.ngt * 32 + 255) / 256;
             LAUNCH(lane_group_terms_kernel, (unsigned)(nbw < (uint64_t)c->sms * 16 ? nbw : c->sms * 16), 256, st,
                    primes, n_dev, n_host, mode, g_sched, L.ngt, gq, (unsigned long long *)(misc + M_LANE_T));
-            const uint64_t nb = (L.ngt + 255) / 256;
-            LAUNCH(lane_slices_kernel, (unsigned)(nb < (uint64_t)c->sms * 8 ? nb : c->sms * 8), 256, st, gq, L.ngt,
+            const uint64_t nb = (L.ngt * 32 + 255) / 256;                 // a warp per group-test
+            LAUNCH(lane_slices_kernel, (unsigned)(nb < (uint64_t)c->sms * 16 ? nb : c->sms * 16), 256, st, gq, L.ngt,
                    L.ntests, recs, K, nch, (const unsigned long long *)(misc + M_LANE_T), lane_items, 4096ull,
-                   LANE_QMAX);
+                   LANE_QMAX, (unsigned long long *)(misc + M_LANE_SLICED));
         }
     }
     TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
@@ -613,6 +615,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
     if (lane) CK(cudaMemcpyAsync(&h[3], gstart + L.ngt, 8, cudaMemcpyDeviceToHost, st));
+    if (lane && lane2) CK(cudaMemcpyAsync(hsl, misc + M_LANE_SLICED, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const uint64_t n = n_dev ? h[0] : n_host;
@@ -635,6 +638,9 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     // batches of <= budget partial pairs, cut at record boundaries (lane mode: at group boundaries, so each
     // batch is whole lane items [hi_[b], hi_[b + 1]))
     const uint64_t budget = part_budget();
+    // most lane groups sliced: every lane item runs the sliced chain code (WV_LANE_ALLSL=0/1 forces it)
+    const char *eas = getenv("WV_LANE_ALLSL");
+    const uint32_t all_sliced = eas ? (uint32_t)atoi(eas) : (2 * hsl[0] > hsl[1] ? 1u : 0u);
     std::vector<uint64_t> hk, hg, hi_;
     if (G <= budget) {
         hk = {0, K};
@@ -681,7 +687,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
             LAUNCH(kVariants[var0].lane, c->sms * c->occ[var0], RES_THREADS, st, recs, start, gstart, gq, L.ngt, ia,
                    ib - ia, L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT),
-                   lane2 ? (unsigned long long *)(misc + M_LANE_TERMS) : nullptr);
+                   lane2 ? (unsigned long long *)(misc + M_LANE_TERMS) : nullptr, all_sliced);
             if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         for (int cls = 0; cls < 3; cls++) {

@@ -595,7 +595,7 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
                      const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
                      uint64_t item_lo, uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
                      ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
-                     unsigned long long *__restrict__ term_count) {
+                     unsigned long long *__restrict__ term_count, uint32_t all_sliced) {
     const uint32_t chain_mask = c_lane_chain;          // bit 0: chain mode for e = 2, bit 1: for e = 3
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -625,12 +625,16 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
         const uint32_t cid0 = __shfl_sync(0xffffffffu, r.cid, vm ? __ffs(vm) - 1 : 0);
         const bool chain = vm && __all_sync(0xffffffffu, !valid || r.cid == cid0) &&
                            ((chain_mask >> (e == 3 ? 2 : 0)) & 1u);
+        // the sliced chain variant (SL) for slices, and for whole groups too when most groups of the launch
+        // are sliced: one hot code path per test instead of two (N-way shards of C2: instruction-fetch
+        // stalls fell from 22 % of the samples; the result is the same, a whole group is slice 0 of 1)
+        const bool sl = Q > 1 || all_sliced;
         if (chain) {
             const Cong &cu = c_cong[cid0];
             // (six-term steps, LaneRunP<3, 6> / <2, 6>, measured slower: C2 residue 17.3 / 15.7 ms vs 13.1)
             // (chains with W pair steps measured slower than without: C2 residue 13.64 vs 13.29 ms; no longer built)
             if (e == 3) {                                  // four-term W steps
-                if (Q > 1) {
+                if (sl) {
                     if (big) lane2_chain_item<RunW, true, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
                     else lane2_chain_item<RunW, false, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
                 } else {
@@ -638,7 +642,7 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
                     else lane2_chain_item<RunW, false, false>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
                 }
             } else {
-                if (Q > 1) {
+                if (sl) {
                     if (big) lane2_chain_item<RunV, true, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
                     else lane2_chain_item<RunV, false, true>(mo, cu, valid, q, Q, rQ, C0, C1, nterms);
                 } else {

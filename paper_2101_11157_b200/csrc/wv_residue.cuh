@@ -289,21 +289,31 @@ __global__ void lane_group_terms_kernel(const uint64_t *__restrict__ primes, con
 __global__ void lane_slices_kernel(uint64_t *__restrict__ gq, uint64_t ngt, uint32_t ntests, const Rec *__restrict__ recs,
                                    uint64_t K, uint64_t *__restrict__ nchunks,
                                    const unsigned long long *__restrict__ lane_total, double items_wanted,
-                                   uint64_t min_slice, uint64_t qmax) {
+                                   uint64_t min_slice, uint64_t qmax, unsigned long long *__restrict__ counts) {
+    // one warp per group-test: lane l owns record (32 g + l) ntests + t.
+    // counts[0] += group-tests cut into Q > 1 slices, counts[1] += lane-mode group-tests
     const double tot = (double)*lane_total;
     uint64_t slice = (uint64_t)ceil(tot / (items_wanted > 1.0 ? items_wanted : 1.0));
     if (slice < min_slice) slice = min_slice;
-    for (uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gt < ngt; gt += (uint64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t gt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gt < ngt; gt += nw) {
         const uint64_t Tl = gq[gt];
-        if (Tl == 0) continue;                       // not a lane-mode group
+        __syncwarp();
+        if (Tl == 0) continue;                       // not a lane-mode group (warp-uniform)
         uint64_t Q = (Tl + slice - 1) / slice;
         if (Q < 1) Q = 1;
         if (Q > qmax) Q = qmax;
-        gq[gt] = Q;
+        if (lane == 0) {
+            gq[gt] = Q;
+            if (counts) {
+                atomicAdd(&counts[1], 1ull);
+                if (Q > 1) atomicAdd(&counts[0], 1ull);
+            }
+        }
         const uint64_t g = gt / ntests, t = gt % ntests;
-        for (uint64_t l = 0; l < 32; l++) {
-            const uint64_t k = (32 * g + l) * ntests + t;
-            if (k >= K) break;
+        const uint64_t k = (32 * g + lane) * ntests + t;
+        if (k < K) {
             const uint64_t p = recs[k].p;
             if (p != 0 && p < WIDTH32_MAX) nchunks[k] = Q;
         }
@@ -1200,7 +1210,8 @@ residue_lane_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ s
                     const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
                     uint64_t item_lo, uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
                     ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
-                    unsigned long long *__restrict__ /*term_count: the plan counts this kernel's terms*/) {
+                    unsigned long long *__restrict__ /*term_count: the plan counts this kernel's terms*/,
+                    uint32_t /*all_sliced: lane2 only*/) {
     using W = typename M::W;
     const int lane = threadIdx.x & 31;
     for (;;) {

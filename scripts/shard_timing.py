@@ -7,7 +7,8 @@ import paper_2101_11157_b200 as wv
 from paper_2101_11157_b200.workloads import CONFIGS
 
 w = CONFIGS["c2"]
-for n in (1, 2, 4, 8):
+ns = [int(x) for x in sys.argv[1:]] or [1, 2, 4, 8]
+for n in ns:
     worst = 0.0
     for shard in range(n):
         ds = wv.DeviceSearch(w.lo, w.hi, w.mode, shard, n)

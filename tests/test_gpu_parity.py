@@ -572,3 +572,19 @@ def test_lane_mode_batches_bit_exact(wv, monkeypatch):
         assert got.n_primes == ref.n_primes
         assert g_res[0].tobytes() == r_res[0].tobytes() and g_res[1].tobytes() == r_res[1].tobytes(), (lo, hi)
         assert got.checksum_int() == r_chk and t_got == t_ref
+
+
+@pytest.mark.parametrize("allsl", ["0", "1"])
+def test_lane2_sliced_code_for_whole_groups(wv, allsl, monkeypatch):
+    """Whole lane groups (Q = 1) give the same bytes through the sliced chain code (a whole group is slice 0
+    of 1) as through the unsliced one: WV_LANE_ALLSL forces either choice; the default picks by launch
+    (most groups sliced -> sliced code for all).  C2 whole and one shard of an 8-way split."""
+    for shard, n in [(0, 1), (5, 8)]:
+        w = CONFIGS["c2"]
+        ref = wv.DeviceSearch(w.lo, w.hi, w.mode, shard, n).run()
+        monkeypatch.setenv("WV_LANE_ALLSL", allsl)
+        got = wv.DeviceSearch(w.lo, w.hi, w.mode, shard, n).run()
+        monkeypatch.delenv("WV_LANE_ALLSL")
+        a, b = ref.res_np(), got.res_np()
+        assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+        assert ref.checksum_int() == got.checksum_int()
