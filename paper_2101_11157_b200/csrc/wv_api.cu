@@ -511,6 +511,30 @@ static int make_layout(uint64_t lo, uint64_t hi, uint32_t mode, uint32_t shard, 
     return WV_OK;
 }
 
+// ------------------------------------------------------------------ lane-mode chain knob
+// WV_LANE_CHAIN (benchmarking / tests: chain mode per exponent, default 5) lives in __constant__ memory of
+// each device; it is rewritten only when the environment value changes, under a lock, stream-ordered
+// before the launch (a value change waits for the stream, so no kernel still running can see it change).
+static std::mutex g_knob_mu;
+static int lane_chain_knob(cudaStream_t st) {
+    static uint32_t cur[64];
+    static bool init[64];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return WV_OK;
+    const char *ev = getenv("WV_LANE_CHAIN");
+    const uint32_t cm = ev ? (uint32_t)strtoul(ev, nullptr, 0) : 5u;
+    std::lock_guard<std::mutex> lk(g_knob_mu);
+    if (!init[dev] || cur[dev] != cm) {
+        CK(cudaDeviceSynchronize());              // no kernel of another stream may be reading the old value
+        CK(cudaMemcpyToSymbolAsync(c_lane_chain, &cm, sizeof cm, 0, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        cur[dev] = cm;
+        init[dev] = true;
+    }
+    return WV_OK;
+}
+
 // ------------------------------------------------------------------ launch helpers
 template <typename T>
 static int scan_excl(const T *in, uint64_t n, uint64_t *out, uint64_t *total, uint64_t *tiles, cudaStream_t st) {
@@ -668,20 +692,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         // unsorted input: every class kernel scans the whole batch and skips the other classes' records
         const uint64_t ia = lane ? hi_[b] : 0, ib = lane ? hi_[b + 1] : 0;
         if (lane && ib > ia) {     // lane mode for class 0: this batch's lane items
-            {   // WV_LANE_CHAIN (benchmarking / tests): chain mode per exponent / W step width, default 5
-                const char *ev = getenv("WV_LANE_CHAIN");
-                static uint32_t cur[64];
-                static bool init[64];
-                int dev = 0;
-                CK(cudaGetDevice(&dev));
-                const uint32_t cm = ev ? (uint32_t)strtoul(ev, nullptr, 0) : 5u;
-                if (dev >= 0 && dev < 64 && (!init[dev] || cur[dev] != cm)) {
-                    CK(cudaMemcpyToSymbolAsync(c_lane_chain, &cm, sizeof cm, 0, cudaMemcpyHostToDevice, st));
-                    CK(cudaStreamSynchronize(st));
-                    cur[dev] = cm;
-                    init[dev] = true;
-                }
-            }
+            TRY(lane_chain_knob(st));
             CK(cudaMemsetAsync(misc + M_CNT, 0, 8, st));
             EvPair ev{nullptr, nullptr, 0};
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }

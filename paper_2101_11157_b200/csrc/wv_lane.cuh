@@ -512,8 +512,10 @@ __device__ __forceinline__ void lane2_chain_item(const MontS &mo, const Cong &cg
             if (b < t) b = t;
             const uint32_t cnt = act ? (uint32_t)(b - t) : 0u;
             const uint32_t ns = cnt / K, r = cnt - ns * K;
-            const uint32_t kmin = __reduce_min_sync(0xffffffffu, valid ? ns : 0xffffffffu);
-            const uint32_t kmax = __reduce_max_sync(0xffffffffu, valid ? ns : 0u);
+            // over the lanes still working: a lane whose slice ended (done) has no terms left and never reads
+            // its run state again, so the unmasked steps may advance it
+            const uint32_t kmin = __reduce_min_sync(0xffffffffu, act ? ns : 0xffffffffu);
+            const uint32_t kmax = __reduce_max_sync(0xffffffffu, act ? ns : 0u);
             uint32_t i = 0;
             #pragma unroll 1
             for (; i + 4 <= kmin; i += 4) {
@@ -596,7 +598,7 @@ residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ 
                      uint64_t item_lo, uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
                      ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
                      unsigned long long *__restrict__ term_count, uint32_t all_sliced) {
-    const uint32_t chain_mask = c_lane_chain;          // bit 0: chain mode for e = 2, bit 1: for e = 3
+    const uint32_t chain_mask = c_lane_chain;          // bit 0: chain mode for e = 2, bit 2: for e = 3
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned long long it = 0;

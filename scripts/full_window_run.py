@@ -34,6 +34,23 @@ out = dict(window=[w.lo, w.hi], name=name, mode=mode, primes=n, hits=ds.hits_np(
            terms=st["terms"], terms_per_s=st["terms"] / (st["residue_ms"] / 1e3), residue_ms=st["residue_ms"],
            hist_chi2_1999dof=chi2, sm_mhz_median=sm[len(sm) // 2] if sm else None, samples=len(sm),
            reasons=sorted(set(c[3].strip() for c in clk if len(c) >= 4)))
+# the oracle goldens of this window (tests/golden/oracle_<name>.npz, written from oracle/ only): every sampled
+# prime's residues as produced by this whole-window run, compared element by element
+gold = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", f"oracle_{name}.npz")
+if os.path.exists(gold):
+    z = np.load(gold)
+    gp = z["p"]
+    pr = ds.primes_np()
+    rw, rv = ds.res_np()
+    idx = np.searchsorted(pr, gp)
+    ok_p = (idx < n) & (pr[np.minimum(idx, n - 1)] == gp)
+    bad = []
+    for t, got, want in (("W", rw, z["res_w"]), ("V", rv, z["res_v"])):
+        if mode & (1 if t == "W" else 2):
+            m = ok_p & (got[np.minimum(idx, n - 1)] != want)
+            bad += [(int(p), t) for p in gp[m]]
+    out["oracle_samples"] = dict(golden=os.path.relpath(gold), samples=int(len(gp)), found=int(ok_p.sum()),
+                                 mismatches=bad)
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open(f"gpurun_out/full_{name}.json", "w"), indent=1)
 print(json.dumps(out))
