@@ -116,12 +116,15 @@ int wv_device_workspace_bytes(uint64_t lo, uint64_t hi, uint32_t mode,
  *   d_workspace           >= wv_device_workspace_bytes(...) bytes, 256-byte aligned
  *                         (NULL: the library allocates it stream-ordered);
  *   stream                a cudaStream_t (NULL = legacy default stream).
- * On return, *n_primes (host) holds the prime count (known after the plan step;
- * the call waits once for it).  With n_hits != NULL, *n_hits holds the hit count
- * and the stream has been synchronised; with n_hits == NULL the call returns as
- * soon as the last kernel is enqueued (hits, residues and checksum are complete
- * when the stream reaches that point; the hit count is not reported).  Returns
- * WV_ENOSPC if prime_cap or workspace_bytes is too small (nothing written). */
+ * n_primes (host, may be NULL): the prime count (known after the plan step; the
+ * call waits once for it).  n_hits (host, may be NULL): the hit count; the stream
+ * is then synchronised.  With both NULL the call may return without waiting at all:
+ * for a window whose primes are all < 2^30 under the default schedule (no
+ * override, stats off) nothing is read back, the item counts stay on the device,
+ * and the call returns once the last kernel is enqueued (hits, residues and
+ * checksum are complete when the stream reaches that point); otherwise it waits
+ * once after the plan step.  Returns WV_ENOSPC if prime_cap or workspace_bytes is
+ * too small (nothing written). */
 int wv_search_device(uint64_t lo, uint64_t hi, uint32_t mode,
                      uint32_t shard, uint32_t nshards, uint64_t block,
                      uint64_t *d_primes, uint64_t *d_res_w, uint64_t *d_res_v,
@@ -255,7 +258,9 @@ int wv_stats_reset(void);
  * kernel ("c0 lane2", default; one prime per lane, sorted prime lists from the
  * sieve) or a chunk kernel (engine, interleaved term streams per lane); for
  * class 1 the K-term FP64 steps ("c1 fp tuples K2/K3", default 6/6) or the
- * term-by-term FP64 / IMAD engines.  wv_kernel_variant_info returns the name
+ * term-by-term FP64 / IMAD engines; for class 2 the K-term 64-bit Montgomery
+ * steps with lazy difference tables ("c2 int tuples K2/K3", default 8/8) or the
+ * term-by-term Mont64 engine ("c2 int s1/1").  wv_kernel_variant_info returns the name
  * and class of variant id (WV_EINVAL past the end); wv_set_kernel_variant
  * selects it for its class (-1 restores the default).  Results are identical
  * for every variant.  Environment knobs read per call (benchmarking only; the
