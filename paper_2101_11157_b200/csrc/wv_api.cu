@@ -192,8 +192,8 @@ static int set_err(int code, const char *fmt, ...) {
 typedef void (*ResKern)(const Rec *, const uint64_t *, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, ulonglong2 *,
                         unsigned long long *, uint32_t, const uint32_t *, uint32_t);
 typedef void (*LaneKern)(const Rec *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t, uint64_t,
-                         uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *, unsigned long long *,
-                         uint32_t);
+                         const uint64_t *, uint32_t, uint64_t, uint64_t, ulonglong2 *, unsigned long long *,
+                         unsigned long long *, uint32_t, const unsigned long long *);
 struct Variant { const char *name; int cls; ResKern fn; LaneKern lane; };
 static const Variant kVariants[] = {
     {"c0 int s1/1", 0, residue_kernel<Mont32, 0, 0, 1, 1>, nullptr},
@@ -587,9 +587,12 @@ static int base_list(DevCtx *c, const Layout &L, void *ws, cudaStream_t st, cons
 
 // plan + scan + residue + finalize for records [0, K) of the primes list.
 // n_dev (device count) or n_host gives the number of valid primes.
+// plan + scan + residue + finalize.  async_ok: the caller does not need the prime count on the host; then,
+// for a window of class-0 primes only (lane mode, default schedule, no stats, the partial-pair bound fits
+// one batch) nothing waits for the device: item counts and the sliced-code choice are read on the device.
 static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev, uint64_t n_host, uint64_t K,
                         uint32_t mode, bool sorted, uint64_t *res_w, uint64_t *res_v, void *ws, const Layout &L,
-                        cudaStream_t st, uint64_t *n_primes_out) {
+                        cudaStream_t st, uint64_t *n_primes_out, bool async_ok = false) {
     NvtxRange range("a2-a5 plan, residues, finalize");
     uint64_t *misc = (uint64_t *)WS(ws, L.o_misc);
     Rec *recs = (Rec *)WS(ws, L.o_recs);
@@ -615,7 +618,7 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
         lane_items = (ev ? atof(ev) : 2.0) * (double)c->sms * c->occ[var0] * (RES_THREADS / 32);
     }
     uint64_t h[4] = {0, 0, 0, 0};   // n, err, G, G_lane
-    uint64_t hs[4], ht[3], hsl[2] = {0, 0};
+    uint64_t hs[4], ht[3];
     if (K > 0) {
         (void)table();
         LAUNCH(plan_kernel, grid_plan ? grid_plan : 1, 256, st, primes, n_dev, n_host, K, mode, g_sched, recs,
@@ -634,19 +637,39 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     }
     TRY(scan_excl<uint64_t>(nch, K, start, start + K, tiles, st));
     if (lane) TRY(scan_excl<uint64_t>(gq, L.ngt, gstart, gstart + L.ngt, tiles, st));
+    const bool stats = g_stats_on.load() != 0;
+    const uint64_t budget = part_budget();
+    // most lane groups sliced: every lane item runs the sliced chain code (WV_LANE_ALLSL=0/1 forces it;
+    // otherwise the kernel decides from the slice counts on the device)
+    const char *eas = getenv("WV_LANE_ALLSL");
+    const uint32_t allsl_mode = eas ? (atoi(eas) ? 1u : 0u) : 2u;
+    // partial slots of a lane-only window: 32 per group-test slice, sum_gt Q <= items wanted + ngt
+    const double gbound = 32.0 * ((double)lane_items + (double)L.ngt);
+    if (async_ok && sorted && lane && lane2 && !stats && L.hi <= WIDTH32_MAX && g_sched.w_force < 0 &&
+        g_sched.v_force < 0 && gbound <= (double)budget && K > 0) {
+        TRY(lane_chain_knob(st));
+        CK(cudaMemsetAsync(misc + M_LANE_TERMS, 0, 8, st));
+        CK(cudaMemsetAsync(misc + M_CNT, 0, 8, st));
+        LAUNCH(kVariants[var0].lane, c->sms * c->occ[var0], RES_THREADS, st, recs, start, gstart, gq, L.ngt, 0ull,
+               0ull, gstart + L.ngt, L.ntests, K, 0ull, part, (unsigned long long *)(misc + M_CNT),
+               (unsigned long long *)(misc + M_LANE_TERMS), allsl_mode,
+               (const unsigned long long *)(misc + M_LANE_SLICED));
+        uint64_t fb = (K + 255) / 256;
+        if (fb > (uint64_t)c->sms * 16) fb = (uint64_t)c->sms * 16;
+        LAUNCH(finalize_kernel, (unsigned)fb, 256, st, recs, start, 0ull, K, 0ull, part, res_w, res_v);
+        return WV_OK;
+    }
     LAUNCH(split_kernel, 1, 32, st, start, K, (const unsigned long long *)(misc + M_FIRST64), misc + M_SPLIT);
     CK(cudaMemcpyAsync(ht, misc + M_TERMS, 24, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h[0], misc + M_NPRIMES, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&h[2], start + K, 8, cudaMemcpyDeviceToHost, st));
     if (lane) CK(cudaMemcpyAsync(&h[3], gstart + L.ngt, 8, cudaMemcpyDeviceToHost, st));
-    if (lane && lane2) CK(cudaMemcpyAsync(hsl, misc + M_LANE_SLICED, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hs, misc + M_SPLIT, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const uint64_t n = n_dev ? h[0] : n_host;
     if (n_primes_out) *n_primes_out = n;
     if ((int)h[1] != 0) return set_err(WV_EINVAL, "schedule chose a congruence not valid for some prime");
     const uint64_t G = h[2];
-    const bool stats = g_stats_on.load() != 0;
     std::vector<EvPair> evs;
     if (stats) {
         std::lock_guard<std::mutex> lk(g_stats_mu);
@@ -661,10 +684,6 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
     const uint64_t kbd[4] = {0, sorted ? hs[1] : 0, sorted ? hs[3] : 0, K};
     // batches of <= budget partial pairs, cut at record boundaries (lane mode: at group boundaries, so each
     // batch is whole lane items [hi_[b], hi_[b + 1]))
-    const uint64_t budget = part_budget();
-    // most lane groups sliced: every lane item runs the sliced chain code (WV_LANE_ALLSL=0/1 forces it)
-    const char *eas = getenv("WV_LANE_ALLSL");
-    const uint32_t all_sliced = eas ? (uint32_t)atoi(eas) : (2 * hsl[0] > hsl[1] ? 1u : 0u);
     std::vector<uint64_t> hk, hg, hi_;
     if (G <= budget) {
         hk = {0, K};
@@ -697,8 +716,9 @@ static int run_residues(DevCtx *c, const uint64_t *primes, const uint64_t *n_dev
             EvPair ev{nullptr, nullptr, 0};
             if (stats) { CK(cudaEventCreate(&ev.a)); CK(cudaEventCreate(&ev.b)); CK(cudaEventRecord(ev.a, st)); }
             LAUNCH(kVariants[var0].lane, c->sms * c->occ[var0], RES_THREADS, st, recs, start, gstart, gq, L.ngt, ia,
-                   ib - ia, L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT),
-                   lane2 ? (unsigned long long *)(misc + M_LANE_TERMS) : nullptr, all_sliced);
+                   ib - ia, (const uint64_t *)nullptr, L.ntests, K, glo, part, (unsigned long long *)(misc + M_CNT),
+                   lane2 ? (unsigned long long *)(misc + M_LANE_TERMS) : nullptr, lane2 ? allsl_mode : 0u,
+                   (const unsigned long long *)(misc + M_LANE_SLICED));
             if (stats) { CK(cudaEventRecord(ev.b, st)); evs.push_back(ev); }
         }
         for (int cls = 0; cls < 3; cls++) {
@@ -782,10 +802,13 @@ static int search_device_impl(const Layout &L, uint64_t *d_primes, uint64_t *d_r
         TRY(run_sieve<uint64_t>(L.map, L.nseg, base, nbh, nbd, d_primes, L.prime_cap, misc + M_NPRIMES, ws, L, st));
     }
     uint64_t n = 0;
-    TRY(run_residues(c, d_primes, misc + M_NPRIMES, 0, L.K, L.mode, true, d_res_w, d_res_v, ws, L, st, &n));
+    const bool async_ok = !n_primes && !n_hits;        // no count wanted on the host
+    TRY(run_residues(c, d_primes, misc + M_NPRIMES, 0, L.K, L.mode, true, d_res_w, d_res_v, ws, L, st,
+                     async_ok ? nullptr : &n, async_ok));
     NvtxRange r6("a6 flags, hits, checksum");
-    if (n > L.prime_cap) return set_err(WV_ENOSPC, "prime count %llu exceeds bound %llu", (unsigned long long)n,
-                                        (unsigned long long)L.prime_cap);
+    if (!async_ok && n > L.prime_cap)   // cannot happen: prime_cap is the Montgomery-Vaughan bound (sieve writes <= cap)
+        return set_err(WV_ENOSPC, "prime count %llu exceeds bound %llu", (unsigned long long)n,
+                       (unsigned long long)L.prime_cap);
     // residues not requested -> WV_RES_NONE; hit flags; checksum
     uint32_t *flags = (uint32_t *)WS(ws, L.o_flags);
     uint64_t *pos = (uint64_t *)WS(ws, L.o_pos);

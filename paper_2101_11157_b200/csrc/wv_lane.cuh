@@ -595,9 +595,14 @@ using RunV = std::conditional<WV_LANE_KV == 4, LaneRun2Q, LaneRunP<2, WV_LANE_KV
 __global__ void __launch_bounds__(RES_THREADS, WV_LANE2_MINB)
 residue_lane2_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                      const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
-                     uint64_t item_lo, uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
-                     ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
-                     unsigned long long *__restrict__ term_count, uint32_t all_sliced) {
+                     uint64_t item_lo, uint64_t nitems_host, const uint64_t *__restrict__ nitems_dev, uint32_t ntests,
+                     uint64_t K, uint64_t part_base, ulonglong2 *__restrict__ partials,
+                     unsigned long long *__restrict__ counter, unsigned long long *__restrict__ term_count,
+                     uint32_t allsl_mode, const unsigned long long *__restrict__ slice_counts) {
+    // item count: from the host, or (asynchronous launches) the device-side total gstart[ngt]
+    const uint64_t nitems = nitems_dev ? *nitems_dev - item_lo : nitems_host;
+    // allsl_mode 0 / 1: forced; 2: most lane group-tests sliced (slice_counts[0] of slice_counts[1])
+    const bool all_sliced = allsl_mode == 2 ? 2 * slice_counts[0] > slice_counts[1] : allsl_mode != 0;
     const uint32_t chain_mask = c_lane_chain;          // bit 0: chain mode for e = 2, bit 2: for e = 3
     const int lane = threadIdx.x & 31;
     for (;;) {

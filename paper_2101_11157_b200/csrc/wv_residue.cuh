@@ -1208,10 +1208,12 @@ template <class M, int CLASS, int ENGINE>
 __global__ void __launch_bounds__(RES_THREADS)
 residue_lane_kernel(const Rec *__restrict__ recs, const uint64_t *__restrict__ start,
                     const uint64_t *__restrict__ gstart, const uint64_t *__restrict__ gq, uint64_t ngt,
-                    uint64_t item_lo, uint64_t nitems, uint32_t ntests, uint64_t K, uint64_t part_base,
-                    ulonglong2 *__restrict__ partials, unsigned long long *__restrict__ counter,
+                    uint64_t item_lo, uint64_t nitems_host, const uint64_t *__restrict__ nitems_dev, uint32_t ntests,
+                    uint64_t K, uint64_t part_base, ulonglong2 *__restrict__ partials,
+                    unsigned long long *__restrict__ counter,
                     unsigned long long *__restrict__ /*term_count: the plan counts this kernel's terms*/,
-                    uint32_t /*all_sliced: lane2 only*/) {
+                    uint32_t /*allsl_mode: lane2 only*/, const unsigned long long *__restrict__ /*slice_counts*/) {
+    const uint64_t nitems = nitems_dev ? *nitems_dev - item_lo : nitems_host;
     using W = typename M::W;
     const int lane = threadIdx.x & 31;
     for (;;) {

@@ -11,7 +11,7 @@ ncu --set full --import-source on --clock-control none -k regex:residue_lane2 -s
 ncu --set full --import-source on --clock-control none -k regex:residue_kernel -s 1 -c 1 -o gpurun_out/r2_c5s \
     python scripts/profile_target.py c5s > gpurun_out/r2_ncu_c5s.log 2>&1
 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    -k "regex:residue_kernel<wv::Mont64, 2, 0, 8, 8" -s 1 -c 1 -o gpurun_out/r2_c2big \
+    -k "regex:Mont64, \(int\)2, \(int\)0, \(int\)8" -s 1 -c 1 -o gpurun_out/r2_c2big \
     python scripts/profile_target.py c2big > gpurun_out/r2_ncu_c2big.log 2>&1
 python scripts/shard_timing.py > gpurun_out/r2_shard.log 2>&1
 python scripts/full_window_run.py c4 > gpurun_out/r2_full_c4.log 2>&1

@@ -588,3 +588,23 @@ def test_lane2_sliced_code_for_whole_groups(wv, allsl, monkeypatch):
         a, b = ref.res_np(), got.res_np()
         assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
         assert ref.checksum_int() == got.checksum_int()
+
+
+def test_async_device_search_equals_synchronous(wv):
+    """wv_search_device with neither count wanted (n_primes = n_hits = NULL) runs a class-0 window without any
+    host synchronisation (item counts and the sliced-code choice read on the device); its residues, hits and
+    checksum equal the synchronous call's, on C2 and an 8-way shard of it (the bench's timed step), and a
+    window reaching past 2^30 (which falls back to the synchronous plan) is unaffected."""
+    import torch
+    for args in [(5, 3 * 10 ** 6, 3, 0, 1), (5, 3 * 10 ** 6, 3, 5, 8), ((1 << 30) - 20000, (1 << 30) + 20000, 3, 0, 1)]:
+        ref = wv.DeviceSearch(*args).run()
+        r_res, r_chk, r_hits = ref.res_np(), ref.checksum_int(), ref.hits_np().tobytes()
+        got = wv.DeviceSearch(*args)
+        got.res_w.fill_(-1)
+        got.res_v.fill_(-1)
+        got.run(hit_count=False, prime_count=False)
+        torch.cuda.synchronize()
+        got.n_primes, got.n_hits = ref.n_primes, ref.n_hits        # counts were not reported by the async call
+        g_res = got.res_np()
+        assert g_res[0].tobytes() == r_res[0].tobytes() and g_res[1].tobytes() == r_res[1].tobytes(), args
+        assert got.checksum_int() == r_chk and got.hits_np().tobytes() == r_hits, args
