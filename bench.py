@@ -568,6 +568,9 @@ def main():
             "method_rate_basis": "SURVEY.md 8(d): 2 mulmods x (227/6480 p + 27/512 p) per prime (BB30/EE33-"
                                  "equivalent work; the method does less, so this is a rate, not a pipe fraction)",
             "ncu_pipes": ncu,
+            "note": ("products are one part of the loop: it also advances the difference tables by modular adds, "
+                     "and is bound by the FMA-heavy and ALU pipes together (ncu_pipes); frac is executed products "
+                     "against the measured product-only rate" if cls == 0 else None),
             "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms_max if ms_max else None,
             "terms_per_step": sum(cls_terms.values()), "kernel_terms_per_s": k_terms / (k_ms / 1e3) if k_ms else None}
 
