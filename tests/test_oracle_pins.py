@@ -275,3 +275,25 @@ def test_prime_counts():
             assert oracle.prime_count(c["lo"], c["hi"]) == c["n"], c
     assert oracle.primes(0, 30) == [2, 3, 5, 7, 11, 13, 17, 19, 23, 29]
     assert oracle.primes(10 ** 9, 10 ** 9 + 2000) == _primes(10 ** 9, 10 ** 9 + 2000)
+
+
+def test_c4_golden_samples_are_the_stated_sample():
+    """tests/golden/oracle_c4.npz holds all 64 samples floor(j*N/64) of the C4 window's primes (the oracle's
+    sieve), each W residue written by scripts/gen_wide_goldens.py from oracle tier B; the duplicates computed
+    on two hosts agree (scripts/data/oracle_wide_cache*.jsonl)."""
+    import glob
+    import numpy as np
+    from paper_2101_11157_b200.workloads import CONFIGS, sample_indices
+    z = np.load(os.path.join(GOLD, "oracle_c4.npz"))
+    meta = json.loads(str(z["meta"]))
+    assert meta["complete"] and meta["samples_present"] == 64
+    w = CONFIGS["c4"]
+    ps = oracle.primes(w.lo, w.hi)
+    assert z["p"].tolist() == [ps[i] for i in sample_indices(len(ps), 64)]
+    vals = {}
+    for path in glob.glob(os.path.join(os.path.dirname(GOLD), "..", "scripts", "data", "oracle_wide_cache*.jsonl")):
+        for line in open(path):
+            d = json.loads(line)
+            vals.setdefault((d["p"], d["test"]), set()).add(d["res"])
+    assert all(len(v) == 1 for v in vals.values())
+    assert [vals[(int(p), "W")].pop() for p in z["p"]] == z["res_w"].tolist()
